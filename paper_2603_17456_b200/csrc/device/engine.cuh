@@ -1,0 +1,2157 @@
+// Device-resident event loop of the flow-level simulator: one warp owns one
+// simulation instance and runs its whole event loop without host round trips.
+//
+// Per processed event (Engine::run, engine.cpp:595-657):
+//   K4  next-event selection: warp argmin over (t, klass, seq) of the arrival
+//       stream head, the small non-flow event pool and the per-active-flow
+//       completion slots (replaces std::priority_queue + stale generations);
+//       streaming `advance_to` over the active SoA (engine.cpp:261-276)
+//   K1  stage-DAG release / admission handlers (engine.cpp:295-593)
+//   K2  RMLQ promotion (rmlq.cpp:101-193, allocator.cpp:128-171)
+//   K3  class construction per policy (baselines.cpp:23-135, rmlq.cpp:201-260)
+//       and strict-priority progressive filling (allocator.cpp:28-126)
+//   K5  MFS Algorithm 1 at batch events (rmlq.cpp:268-382, inter_request.cpp)
+//
+// Exactness: every FP operation that the reference performs is performed here
+// in the same order with IEEE double round-to-nearest and no contraction
+// (built with -fmad=false; critical spots use __d*_rn explicitly). Decisions
+// that the reference takes in container order (active_ swap-remove order,
+// push seq numbering, unordered_map iteration in load_fraction) are replayed.
+#pragma once
+#include <math.h>
+#include <stdint.h>
+#if !defined(__CUDACC__)
+#include <string.h>
+#endif
+
+#include "lanes.cuh"
+#include "layout.h"
+
+namespace mfb {
+
+#define MF_INF (__builtin_huge_val())
+constexpr double kNoTime = -1.0;
+constexpr unsigned long long kNoSeq = ~0ull;
+
+// libstdc++ _Prime_rehash_policy schedule for an unordered_map grown one
+// insertion at a time from empty (measured; see oracle/hash_schedule.cpp).
+constexpr int kHashStages = 19;
+#if defined(__CUDACC__)
+__device__ __constant__ int kRehashAt[kHashStages] = {
+#else
+static const int kRehashAt[kHashStages] = {
+#endif
+    0,     13,     29,     59,     127,    257,    541,     1109,    2357,   5087,
+    10273, 20753,  42043,  85229,  172933, 351061, 712697,  1447153, 2938679};
+#if defined(__CUDACC__)
+__device__ __constant__ int kBucketsAt[kHashStages] = {
+#else
+static const int kBucketsAt[kHashStages] = {
+#endif
+    13,    29,     59,     127,    257,    541,     1109,    2357,    5087,   10273,
+    20753, 42043,  85229,  172933, 351061, 712697,  1447153, 2938679, 5967347};
+
+// ---------------------------------------------------------------------------
+// IEEE helpers (std::min / std::max argument-order semantics)
+
+MF_FN double smin(double a, double b) { return (b < a) ? b : a; }
+MF_FN double smax(double a, double b) { return (a < b) ? b : a; }
+#if defined(__CUDACC__)
+MF_FN double dmul(double a, double b) { return __dmul_rn(a, b); }
+MF_FN double dadd(double a, double b) { return __dadd_rn(a, b); }
+MF_FN double dsub(double a, double b) { return __dsub_rn(a, b); }
+MF_FN double ddiv(double a, double b) { return __ddiv_rn(a, b); }
+MF_FN unsigned long long dbits(double x) { return (unsigned long long)__double_as_longlong(x); }
+MF_FN bool isnan_(double x) { return isnan(x); }
+#else
+MF_FN double dmul(double a, double b) { return a * b; }
+MF_FN double dadd(double a, double b) { return a + b; }
+MF_FN double dsub(double a, double b) { return a - b; }
+MF_FN double ddiv(double a, double b) { return a / b; }
+MF_FN unsigned long long dbits(double x) {
+  unsigned long long u;
+  memcpy(&u, &x, 8);
+  return u;
+}
+MF_FN bool isnan_(double x) { return x != x; }
+#endif
+// order-preserving map double -> u64 (non-NaN; -0 folded onto +0)
+MF_FN unsigned long long dord(double x) {
+  if (x == 0.0) x = 0.0;
+  unsigned long long u = dbits(x);
+  return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
+}
+MF_FN int klass_of(int kind) { return kind <= EV_DEPART ? 0 : (kind == EV_TICK ? 2 : 1); }
+MF_FN int pow2ceil(int n) {
+  int p = 1;
+  while (p < n) p <<= 1;
+  return p;
+}
+
+// Scalar state: every lane keeps an identical register copy.
+struct Sc {
+  double now;
+  double prev_t;
+  double horizon;
+  unsigned long long seq;
+  long long events, steps, streak, pushes, algo_bytes, classes, rounds;
+  int n_flows, n_batches, n_coflows, n_active, n_ev;
+  int rp_top, pp_top, cm_top;
+  int next_arr;
+  unsigned epoch;
+  int n_live;
+  int h_n, h_ready;
+  int dirty;
+  int err, chk;
+  long long pruned;
+  int max_active;
+};
+
+struct Ev {
+  double t;
+  int klass;
+  unsigned long long seq;
+  int src;  // 0 none, 1 arrival, 2 pool, 3 flow slot
+  int idx;
+};
+
+MF_FN bool ev_less(const Ev& x, const Ev& y) {
+  if (x.t != y.t) return x.t < y.t;
+  if (x.klass != y.klass) return x.klass < y.klass;
+  return x.seq < y.seq;
+}
+
+template <class G>
+struct Engine {
+  G g;
+  const Inst& I;
+  Sc s;
+
+  MF_FN explicit Engine(const Inst& inst) : I(inst) {}
+
+  // ----------------------------------------------------------------- util
+  template <class T>
+  MF_FN void put(T* p, T v) { g.put(p, v); }
+  MF_FN void fail(int code, int chk) {
+    if (!s.err) {
+      s.err = code;
+      s.chk = chk;
+    }
+  }
+  MF_FN int rbeg(int fid) const { return I.route_off[I.f_route[fid]]; }
+  MF_FN int rlen(int fid) const {
+    int r = I.f_route[fid];
+    return I.route_off[r + 1] - I.route_off[r];
+  }
+  MF_FN bool done(int fid) const { return I.f_state[fid] == FL_DONE; }
+  MF_FN double remaining(int fid) const {
+    int p = I.f_apos[fid];
+    if (p >= 0) return I.a_rem[p];
+    return I.f_state[fid] == FL_DONE ? 0.0 : I.f_size[fid];
+  }
+  MF_FN bool has_dl(int fid) const { return !isnan_(I.f_dl[fid]); }
+  MF_FN bool outranks(int ba, int la, int bb, int lb) const {
+    if (ba != bb) return ba < bb;
+    return la < lb;
+  }
+
+  // ------------------------------------------------------------ event pool
+  MF_FN void push(double t, int kind, int a, int b) {
+    if (s.n_ev >= I.E_cap) {
+      fail(ERR_INTERNAL, CHK_CAP_EVENTS);
+      return;
+    }
+    const int i = s.n_ev;
+    g.sync();
+    if (g.leader()) {
+      I.e_t[i] = t;
+      I.e_seq[i] = s.seq;
+      I.e_kind[i] = kind;
+      I.e_a[i] = a;
+      I.e_b[i] = b;
+    }
+    g.sync();
+    ++s.n_ev;
+    ++s.seq;
+    ++s.pushes;
+  }
+
+  MF_FN Ev next_event() {
+    Ev best;
+    best.t = MF_INF;
+    best.klass = 3;
+    best.seq = kNoSeq;
+    best.src = 0;
+    best.idx = -1;
+    if (g.leader() && s.next_arr < I.n_arr) {
+      int r = I.arr_order[s.next_arr];
+      Ev c{I.r_arrival[r], 1, (unsigned long long)r, 1, r};
+      best = c;
+    }
+    for (int i = g.lane(); i < s.n_ev; i += G::N) {
+      Ev c{I.e_t[i], klass_of(I.e_kind[i]), I.e_seq[i], 2, i};
+      if (best.src == 0 || ev_less(c, best)) best = c;
+    }
+    for (int p = g.lane(); p < s.n_active; p += G::N) {
+      unsigned long long q = I.a_evseq[p];
+      if (q == kNoSeq) continue;
+      Ev c{I.a_evt[p], 0, q, 3, p};
+      if (best.src == 0 || ev_less(c, best)) best = c;
+    }
+    for (int m = G::N / 2; m > 0; m >>= 1) {
+      Ev o;
+      o.t = g.shfl_xor(best.t, m);
+      o.klass = g.shfl_xor(best.klass, m);
+      o.seq = g.shfl_xor(best.seq, m);
+      o.src = g.shfl_xor(best.src, m);
+      o.idx = g.shfl_xor(best.idx, m);
+      if (o.src != 0 && (best.src == 0 || ev_less(o, best))) best = o;
+    }
+    s.algo_bytes += 16LL * s.n_active + 24LL * s.n_ev;
+    return best;
+  }
+
+  MF_FN void pool_remove(int i) {
+    const int last = s.n_ev - 1;
+    g.sync();
+    if (g.leader() && i != last) {
+      I.e_t[i] = I.e_t[last];
+      I.e_seq[i] = I.e_seq[last];
+      I.e_kind[i] = I.e_kind[last];
+      I.e_a[i] = I.e_a[last];
+      I.e_b[i] = I.e_b[last];
+    }
+    g.sync();
+    --s.n_ev;
+  }
+
+  // ----------------------------------------------------- active flow set
+  MF_FN void remove_active(int fid) {  // engine.cpp:251-259
+    const int pos = I.f_apos[fid];
+    if (pos < 0) return;
+    const int last = s.n_active - 1;
+    const int lf = I.a_fid[last];
+    g.sync();
+    if (g.leader()) {
+      I.a_fid[pos] = lf;
+      I.a_rem[pos] = I.a_rem[last];
+      I.a_rate[pos] = I.a_rate[last];
+      I.a_evt[pos] = I.a_evt[last];
+      I.a_evseq[pos] = I.a_evseq[last];
+      I.f_apos[lf] = pos;
+      I.f_apos[fid] = -1;
+    }
+    g.sync();
+    --s.n_active;
+  }
+
+  MF_FN void advance_to(double t) {  // engine.cpp:261-276
+    const double dt = dsub(t, s.now);
+    if (!(dt > -1e-9)) {
+      fail(ERR_INTERNAL, CHK_TIME_BACKWARDS);
+      return;
+    }
+    if (dt > 0.0) {
+      bool bad = false;
+      for (int p = g.lane(); p < s.n_active; p += G::N) {
+        double rem = dsub(I.a_rem[p], dmul(I.a_rate[p], dt));
+        if (rem < 0.0) {
+          double sz = I.f_size[I.a_fid[p]];
+          if (!(rem > dsub(-dmul(1e-6, smax(sz, 1.0)), 1e-9))) bad = true;
+          rem = 0.0;
+        }
+        I.a_rem[p] = rem;
+      }
+      g.sync();
+      s.algo_bytes += 24LL * s.n_active;
+      if (g.any(bad)) {
+        fail(ERR_INTERNAL, CHK_OVERSHOOT);
+        return;
+      }
+    }
+    s.now = t;
+  }
+
+  // --------------------------------------------------------- pipeline info
+  MF_FN int l_curr(int b) const {  // engine.cpp:712-720
+    const int L = I.b_layers[b];
+    const int base = I.b_lbase[b];
+    for (int l = 1; l <= L; ++l) {
+      int idx = base + l - 1;
+      if (!I.pl_done[idx]) return l;
+      int c = I.pl_coll[idx];
+      if (c >= 0 && I.c_open[c] > 0) return l;
+    }
+    return L > 1 ? L : 1;
+  }
+  MF_FN double remaining_compute(int b) const {  // engine.cpp:722-728
+    const int L = I.b_layers[b];
+    const int base = I.b_lbase[b];
+    double total = 0.0;
+    for (int i = 0; i < L; ++i)
+      if (!I.pl_done[base + i]) total = dadd(total, I.pl_cost[base + i]);
+    return total;
+  }
+  MF_FN bool batch_drained(int b) const {  // engine.cpp:730-734
+    return I.b_done[b] != kNoTime && I.b_open[b] == 0;
+  }
+
+  // ========================================================= K2: RMLQ
+  MF_FN int mlu_level(double v) {  // rmlq.cpp:29-34
+    if (!(v >= 0.0)) {
+      fail(ERR_INTERNAL, CHK_NEG_MLU);
+      return I.p.K;
+    }
+    for (int i = 1; i <= I.p.K - 1; ++i)
+      if (v >= I.p.thr[i - 1]) return i;
+    return I.p.K;
+  }
+
+  // LinkLoadIndex (allocator.cpp:143-161): entries (link, band<<16|level, rate)
+  // for allocated flows with rate > 0, sorted, prefix sums per link.
+  MF_NOINLINE int build_index() {
+    // count entries
+    int total = 0;
+    for (int base = 0; base < s.n_active; base += G::N) {
+      int p = base + g.lane();
+      int c = 0;
+      if (p < s.n_active && I.a_rate[p] > 0.0) c = rlen(I.a_fid[p]);
+      int tot;
+      int off = g.excl_scan(c, &tot);
+      if (c > 0) {
+        int fid = I.a_fid[p];
+        int rb = rbeg(fid);
+        unsigned long long key = ((unsigned long long)I.f_band[fid] << 16) | I.f_level[fid];
+        double r = I.a_rate[p];
+        for (int k = 0; k < c; ++k) {
+          int l = I.route_links[rb + k];
+          I.x_hi[total + off + k] = ((unsigned long long)l << 32) | key;
+          I.x_lo[total + off + k] = dbits(r);
+          I.x_val[total + off + k] = r;
+        }
+      }
+      total += tot;
+    }
+    g.sync();
+    if (total > I.X_cap) {
+      fail(ERR_INTERNAL, CHK_CAP_SCRATCH);
+      return 0;
+    }
+    sort_x(total);
+    // segment heads -> sequential prefix sums per link segment
+    int nseg = 0;
+    for (int base = 0; base < total; base += G::N) {
+      int i = base + g.lane();
+      int h = 0;
+      if (i < total) h = (i == 0 || (I.x_hi[i] >> 32) != (I.x_hi[i - 1] >> 32)) ? 1 : 0;
+      int tot;
+      int off = g.excl_scan(h, &tot);
+      if (h) I.x_seg[nseg + off] = i;
+      nseg += tot;
+    }
+    g.sync();
+    for (int k = g.lane(); k < nseg; k += G::N) {
+      int i0 = I.x_seg[k];
+      int i1 = (k + 1 < nseg) ? I.x_seg[k + 1] : total;
+      double run = 0.0;
+      for (int i = i0; i < i1; ++i) {
+        run = dadd(run, I.x_val[i]);
+        I.x_pre[i] = run;
+      }
+    }
+    g.sync();
+    s.algo_bytes += 40LL * total;
+    return total;
+  }
+
+  // LinkLoadIndex::higher_fraction (allocator.cpp:163-171); per-lane query
+  MF_FN double index_fraction(int nx, int l, int band, int level) const {
+    unsigned long long want = ((unsigned long long)l << 32) |
+                              (((unsigned long long)band << 16) | (unsigned long long)level);
+    // first entry with hi >= want
+    int lo = 0, hi = nx;
+    while (lo < hi) {
+      int mid = (lo + hi) >> 1;
+      if (I.x_hi[mid] < want)
+        lo = mid + 1;
+      else
+        hi = mid;
+    }
+    if (lo == 0 || (I.x_hi[lo - 1] >> 32) != (unsigned long long)l) return 0.0;
+    double load = I.x_pre[lo - 1];
+    double v = ddiv(load, I.cap[l]);
+    return v < 0.0 ? 0.0 : (1.0 < v ? 1.0 : v);
+  }
+
+  // libstdc++ iteration order of the last allocation's rate map
+  MF_NOINLINE void build_hash_order() {
+    const int n = s.h_n;
+    if (g.leader()) {
+      int head = -1;
+      int bc = 1;
+      int stage = 0;
+      for (int i = 0; i < n; ++i) {
+        if (stage < kHashStages && i == kRehashAt[stage]) {
+          int nbc = kBucketsAt[stage++];
+          for (int b = 0; b < nbc; ++b) I.h_bkt[b] = -2;
+          int p = head;
+          head = -1;
+          int bbegin = -1;
+          while (p != -1) {
+            int nx = I.h_next[p];
+            int b = I.h_keys[p] % nbc;
+            if (I.h_bkt[b] == -2) {
+              I.h_next[p] = head;
+              head = p;
+              I.h_bkt[b] = -1;
+              if (I.h_next[p] != -1) I.h_bkt[bbegin] = p;
+              bbegin = b;
+            } else {
+              int a = I.h_bkt[b];
+              if (a == -1) {
+                I.h_next[p] = head;
+                head = p;
+              } else {
+                I.h_next[p] = I.h_next[a];
+                I.h_next[a] = p;
+              }
+            }
+            p = nx;
+          }
+          bc = nbc;
+        }
+        int b = I.h_keys[i] % bc;
+        if (I.h_bkt[b] != -2) {
+          int a = I.h_bkt[b];
+          if (a == -1) {
+            I.h_next[i] = head;
+            head = i;
+          } else {
+            I.h_next[i] = I.h_next[a];
+            I.h_next[a] = i;
+          }
+        } else {
+          I.h_next[i] = head;
+          head = i;
+          if (I.h_next[i] != -1) I.h_bkt[I.h_keys[I.h_next[i]] % bc] = i;
+          I.h_bkt[b] = -1;
+        }
+      }
+      int rank = 0;
+      for (int p = head; p != -1; p = I.h_next[p]) I.h_rank[p] = rank++;
+    }
+    g.sync();
+    s.h_ready = 1;
+  }
+
+  // load_fraction (allocator.cpp:128-141): sum in unordered_map order
+  MF_NOINLINE double load_fraction(int l, int band, int level) {
+    int cnt = 0;
+    for (int base = 0; base < s.n_active; base += G::N) {
+      int p = base + g.lane();
+      int c = 0;
+      if (p < s.n_active && I.a_rate[p] > 0.0) {
+        int fid = I.a_fid[p];
+        if (outranks(I.f_band[fid], I.f_level[fid], band, level)) {
+          int rb = rbeg(fid), rn = rlen(fid);
+          for (int k = 0; k < rn; ++k)
+            if (I.route_links[rb + k] == l) {
+              c = 1;
+              break;
+            }
+        }
+      }
+      int tot;
+      int off = g.excl_scan(c, &tot);
+      if (c) {
+        int fid = I.a_fid[p];
+        I.x_hi[cnt + off] = (unsigned long long)I.f_hidx[fid];
+        I.x_lo[cnt + off] = 0;
+        I.x_val[cnt + off] = I.a_rate[p];
+      }
+      cnt += tot;
+    }
+    g.sync();
+    s.algo_bytes += 24LL * s.n_active;
+    double used = 0.0;
+    if (cnt <= 2) {
+      for (int i = 0; i < cnt; ++i) used = dadd(used, I.x_val[i]);
+    } else {
+      if (!s.h_ready) build_hash_order();
+      for (int i = g.lane(); i < cnt; i += G::N)
+        I.x_hi[i] = (unsigned long long)I.h_rank[(int)I.x_hi[i]];
+      g.sync();
+      sort_x(cnt);
+      for (int i = 0; i < cnt; ++i) used = dadd(used, I.x_val[i]);
+    }
+    double v = ddiv(used, I.cap[l]);
+    return v < 0.0 ? 0.0 : (1.0 < v ? 1.0 : v);
+  }
+
+  // natural_key (rmlq.cpp:101-127) -> (band, level); per-lane when idx given
+  MF_FN void natural_key(int fid, int lcur, int nx, bool use_idx, int* ob, int* ol) {
+    const int st = I.f_stage[fid];
+    if (st != ST_P2D) {
+      int v = I.f_tl[fid] - lcur;
+      if (v < 0) v = 0;
+      if (v > I.p.K - 1) v = I.p.K - 1;
+      *ob = BD_EARLY;
+      *ol = v + 1;
+      return;
+    }
+    int pb = I.f_band[fid], pl = I.f_level[fid];
+    if (pb == BD_EARLY) {
+      pb = BD_DEFERRED;
+      pl = I.p.K;
+    }
+    // compute_mlu (rmlq.cpp:43-82)
+    const double size_rem = remaining(fid);
+    const double time_rem = dsub(I.f_dl[fid], s.now);
+    const int rn = rlen(fid), rb = rbeg(fid);
+    double value;
+    if (rn == 0) {
+      value = 0.0;
+    } else {
+      double best_eff = MF_INF;
+      for (int k = 0; k < rn; ++k) {
+        int l = I.route_links[rb + k];
+        double rho = use_idx ? index_fraction(nx, l, pb, pl) : load_fraction(l, pb, pl);
+        double eff = dmul(I.cap[l], dsub(1.0, rho));
+        if (eff < best_eff) best_eff = eff;
+      }
+      if (size_rem <= 0.0)
+        value = 0.0;
+      else if (time_rem <= 0.0)
+        value = MF_INF;
+      else if (best_eff <= 0.0)
+        value = MF_INF;
+      else
+        value = ddiv(size_rem, dmul(time_rem, best_eff));
+    }
+    int lv;
+    if (!(value >= 0.0)) {
+      lv = I.p.K;  // flagged below by the caller's check
+      *ol = -1;
+      *ob = BD_DEFERRED;
+      return;
+    }
+    lv = I.p.K;
+    for (int i = 1; i <= I.p.K - 1; ++i)
+      if (value >= I.p.thr[i - 1]) {
+        lv = i;
+        break;
+      }
+    *ol = lv;
+    *ob = lv == 1 ? BD_URGENT : BD_DEFERRED;
+  }
+
+  MF_FN int rank_of(int fid) const {  // rmlq.cpp:89-99
+    int r = I.f_req[fid];
+    if (r >= 0 && I.r_rank[r] >= 0) return I.r_rank[r];
+    int b = I.f_batch[fid];
+    if (b >= 0 && I.b_rank[b] >= 0) return I.b_rank[b];
+    return 0;
+  }
+
+  MF_FN void on_flow_released(int fid) {  // rmlq.cpp:137-148
+    if (I.p.policy != POL_MFS) return;
+    const int r = I.f_req[fid];
+    if (r >= 0 && I.r_pruned[r]) {
+      g.sync();
+      if (g.leader()) {
+        I.f_band[fid] = BD_SCAV;
+        I.f_level[fid] = (uint8_t)I.p.K;
+      }
+      g.sync();
+      return;
+    }
+    const int b = I.f_batch[fid];
+    const int lcur = b >= 0 ? l_curr(b) : 1;
+    int nb, nl;
+    natural_key(fid, lcur, 0, false, &nb, &nl);
+    if (nl < 0) {
+      fail(ERR_INTERNAL, CHK_NEG_MLU);
+      return;
+    }
+    const int rk = rank_of(fid);
+    g.sync();
+    if (g.leader()) {
+      I.f_band[fid] = (uint8_t)nb;
+      I.f_level[fid] = (uint8_t)nl;
+      I.f_rank[fid] = rk;
+    }
+    g.sync();
+    if (nb == BD_URGENT && I.f_stage[fid] != ST_P2D) fail(ERR_INTERNAL, CHK_URGENT_BAND);
+  }
+
+  // promote over a batch (rmlq.cpp:150-193); p2d_only for the periodic tick
+  MF_NOINLINE bool promote_batch(int b, bool p2d_only) {
+    const int nx = build_index();
+    if (s.err) return false;
+    const int lcur = l_curr(b);
+    const int f0 = I.b_ffirst[b], fc = I.b_fcount[b];
+    bool changed = false, bad = false, urgent_bad = false;
+    for (int i = g.lane(); i < fc; i += G::N) {
+      const int fid = f0 + i;
+      const int stt = I.f_state[fid];
+      if (stt == FL_DONE || stt == FL_PRUNED) continue;
+      if (p2d_only && I.f_stage[fid] != ST_P2D) continue;
+      if (I.f_band[fid] == BD_SCAV) continue;
+      int nb, nl;
+      natural_key(fid, lcur, nx, true, &nb, &nl);
+      if (nl < 0) {
+        bad = true;
+        continue;
+      }
+      if (!outranks(nb, nl, I.f_band[fid], I.f_level[fid])) continue;
+      I.f_band[fid] = (uint8_t)nb;
+      I.f_level[fid] = (uint8_t)nl;
+      if (nb == BD_URGENT && I.f_stage[fid] != ST_P2D) urgent_bad = true;
+      changed = true;
+    }
+    g.sync();
+    s.algo_bytes += 40LL * fc;
+    if (g.any(bad)) fail(ERR_INTERNAL, CHK_NEG_MLU);
+    if (g.any(urgent_bad)) fail(ERR_INTERNAL, CHK_URGENT_BAND);
+    return g.any(changed);
+  }
+
+  MF_FN void on_layer_boundary(int b) {
+    if (I.p.policy != POL_MFS) return;
+    promote_batch(b, false);
+  }
+
+  // ==================================================== sorting (warp bitonic)
+  MF_FN bool pos_less(int pa, int pb) const {
+    if (pb < 0) return pa >= 0;
+    if (pa < 0) return false;
+    if (I.s_k0[pa] != I.s_k0[pb]) return I.s_k0[pa] < I.s_k0[pb];
+    if (I.s_k1[pa] != I.s_k1[pb]) return I.s_k1[pa] < I.s_k1[pb];
+    if (I.s_k2[pa] != I.s_k2[pb]) return I.s_k2[pa] < I.s_k2[pb];
+    if (I.s_k3[pa] != I.s_k3[pb]) return I.s_k3[pa] < I.s_k3[pb];
+    return I.a_fid[pa] < I.a_fid[pb];
+  }
+  MF_FN bool pos_same_class(int pa, int pb) const {
+    return I.s_k0[pa] == I.s_k0[pb] && I.s_k1[pa] == I.s_k1[pb] && I.s_k2[pa] == I.s_k2[pb] &&
+           I.s_k3[pa] == I.s_k3[pb];
+  }
+  MF_FN void sort_ord(int* ord, int n) {
+    if (n <= 1) return;
+    const int n2 = pow2ceil(n);
+    for (int i = n + g.lane(); i < n2; i += G::N) ord[i] = -1;
+    g.sync();
+    for (int k = 2; k <= n2; k <<= 1) {
+      for (int j = k >> 1; j > 0; j >>= 1) {
+        for (int i = g.lane(); i < n2; i += G::N) {
+          int ixj = i ^ j;
+          if (ixj > i) {
+            int a = ord[i], b = ord[ixj];
+            bool up = (i & k) == 0;
+            if (up ? pos_less(b, a) : pos_less(a, b)) {
+              ord[i] = b;
+              ord[ixj] = a;
+            }
+          }
+        }
+        g.sync();
+      }
+    }
+  }
+  // joint sort of x_hi/x_lo/x_val by (hi, lo)
+  MF_FN void sort_x(int n) {
+    if (n <= 1) return;
+    const int n2 = pow2ceil(n);
+    for (int i = n + g.lane(); i < n2; i += G::N) {
+      I.x_hi[i] = ~0ull;
+      I.x_lo[i] = ~0ull;
+      I.x_val[i] = 0.0;
+    }
+    g.sync();
+    for (int k = 2; k <= n2; k <<= 1) {
+      for (int j = k >> 1; j > 0; j >>= 1) {
+        for (int i = g.lane(); i < n2; i += G::N) {
+          int ixj = i ^ j;
+          if (ixj > i) {
+            unsigned long long ah = I.x_hi[i], al = I.x_lo[i];
+            unsigned long long bh = I.x_hi[ixj], bl = I.x_lo[ixj];
+            bool b_less = bh < ah || (bh == ah && bl < al);
+            bool a_less = ah < bh || (ah == bh && al < bl);
+            bool up = (i & k) == 0;
+            if (up ? b_less : a_less) {
+              double av = I.x_val[i];
+              I.x_hi[i] = bh;
+              I.x_lo[i] = bl;
+              I.x_val[i] = I.x_val[ixj];
+              I.x_hi[ixj] = ah;
+              I.x_lo[ixj] = al;
+              I.x_val[ixj] = av;
+            }
+          }
+        }
+        g.sync();
+      }
+    }
+  }
+
+  // group s_ord[o0, o0+n) into classes of equal keys, appending to s_cls
+  MF_FN int group_classes(int o0, int n, int ncls) {
+    for (int base = 0; base < n; base += G::N) {
+      int i = base + g.lane();
+      int h = 0;
+      if (i < n) h = (i == 0 || !pos_same_class(I.s_ord[o0 + i], I.s_ord[o0 + i - 1])) ? 1 : 0;
+      int tot;
+      int off = g.excl_scan(h, &tot);
+      if (h) I.s_cls[ncls + off] = o0 + i;
+      ncls += tot;
+    }
+    g.sync();
+    return ncls;
+  }
+
+  // compact active positions satisfying pred (in active order) into ord
+  template <class P>
+  MF_FN int compact(int* ord, P pred) {
+    int n = 0;
+    for (int base = 0; base < s.n_active; base += G::N) {
+      int p = base + g.lane();
+      int c = (p < s.n_active && pred(p)) ? 1 : 0;
+      int tot;
+      int off = g.excl_scan(c, &tot);
+      if (c) ord[n + off] = p;
+      n += tot;
+    }
+    g.sync();
+    return n;
+  }
+
+  // ================================================= K3: decide (policies)
+  // Fills s_ord (class order of active positions), s_cls (class starts, with
+  // sentinel) and s_cap; returns the number of classes and *has_caps.
+  MF_NOINLINE int decide(bool* has_caps) {
+    *has_caps = false;
+    const int A = s.n_active;
+    if (A == 0) return 0;
+    const int pol = I.p.policy;
+    int ncls = 0;
+    if (pol == POL_FS) {  // baselines.cpp:46-51
+      for (int p = g.lane(); p < A; p += G::N) I.s_ord[p] = p;
+      g.sync();
+      I.s_cls[0] = 0;  // benign identical writes
+      ncls = 1;
+    } else if (pol == POL_SJF) {  // baselines.cpp:23-57
+      for (int p = g.lane(); p < A; p += G::N) {
+        int fid = I.a_fid[p];
+        I.s_ord[p] = p;
+        I.s_k0[p] = dord(I.a_rem[p]);
+        I.s_k1[p] = dord(I.f_rel[fid]);
+        I.s_k2[p] = 0;
+        I.s_k3[p] = 0;
+      }
+      g.sync();
+      sort_ord(I.s_ord, A);
+      ncls = group_classes(0, A, 0);
+    } else if (pol == POL_EDF) {  // baselines.cpp:59-90
+      int ne = compact(I.s_ord, [&](int p) { return has_dl(I.a_fid[p]); });
+      for (int i = g.lane(); i < ne; i += G::N) {
+        int p = I.s_ord[i];
+        int fid = I.a_fid[p];
+        I.s_k0[p] = dord(I.f_dl[fid]);
+        I.s_k1[p] = dord(I.f_rel[fid]);
+        I.s_k2[p] = 0;
+        I.s_k3[p] = 0;
+      }
+      g.sync();
+      sort_ord(I.s_ord, ne);
+      ncls = group_classes(0, ne, 0);
+      int ni = compact(I.s_ord + ne, [&](int p) { return !has_dl(I.a_fid[p]); });
+      if (ni > 0) {
+        if (g.leader()) I.s_cls[ncls] = ne;
+        g.sync();
+        ++ncls;
+      }
+    } else if (pol == POL_KARUNA) {  // baselines.cpp:92-135
+      int nd = compact(I.s_ord, [&](int p) { return has_dl(I.a_fid[p]); });
+      if (nd > 0) {
+        karuna_caps(nd);
+        if (s.err) return 0;
+        *has_caps = true;
+        if (g.leader()) I.s_cls[0] = 0;
+        g.sync();
+        ncls = 1;
+      }
+      int nr = compact(I.s_ord + nd, [&](int p) { return !has_dl(I.a_fid[p]); });
+      for (int i = g.lane(); i < nr; i += G::N) {
+        int p = I.s_ord[nd + i];
+        I.s_k0[p] = dord(I.a_rem[p]);
+        I.s_k1[p] = dord(I.f_rel[I.a_fid[p]]);
+        I.s_k2[p] = 0;
+        I.s_k3[p] = 0;
+      }
+      g.sync();
+      sort_ord(I.s_ord + nd, nr);
+      ncls = group_classes(nd, nr, ncls);
+    } else {  // MFS arbitrate (rmlq.cpp:201-260)
+      for (int p = g.lane(); p < A; p += G::N) {
+        int fid = I.a_fid[p];
+        int band = I.f_band[fid];
+        double dl = I.f_dl[fid];
+        if (isnan_(dl)) {
+          int r = I.f_req[fid];
+          dl = r >= 0 ? I.r_deadline[r] : MF_INF;
+        }
+        double k1 = 0.0, k2 = 0.0, k3 = 0.0;
+        if (band == BD_URGENT || band == BD_DEFERRED) {
+          k1 = (double)I.f_level[fid];
+          k2 = dl;
+        } else if (band == BD_EARLY) {
+          k1 = (double)I.f_level[fid];
+          k2 = (double)I.f_rank[fid];
+          k3 = I.f_rel[fid];
+        } else {
+          k1 = dl;
+        }
+        I.s_ord[p] = p;
+        I.s_k0[p] = (unsigned long long)band;
+        I.s_k1[p] = dord(k1);
+        I.s_k2[p] = dord(k2);
+        I.s_k3[p] = dord(k3);
+      }
+      g.sync();
+      sort_ord(I.s_ord, A);
+      ncls = group_classes(0, A, 0);
+    }
+    if (g.leader()) I.s_cls[ncls] = A;
+    g.sync();
+    s.algo_bytes += 40LL * A;
+    return ncls;
+  }
+
+  // Karuna caps for the deadline class s_ord[0, nd): per-link demand summed in
+  // active order (baselines.cpp:102-133).
+  MF_NOINLINE void karuna_caps(int nd) {
+    const int A = s.n_active;
+    for (int p = g.lane(); p < A; p += G::N) I.s_cap[p] = MF_INF;
+    g.sync();
+    // entries (link, active position) for flows with a positive slack
+    int total = 0;
+    for (int base = 0; base < nd; base += G::N) {
+      int i = base + g.lane();
+      int c = 0;
+      int p = -1, fid = -1;
+      double want = 0.0;
+      if (i < nd) {
+        p = I.s_ord[i];
+        fid = I.a_fid[p];
+        double slack = dsub(I.f_dl[fid], s.now);
+        if (slack > 0.0) {
+          want = ddiv(I.a_rem[p], slack);
+          c = rlen(fid);
+        }
+      }
+      int tot;
+      int off = g.excl_scan(c, &tot);
+      if (c > 0) {
+        int rb = rbeg(fid);
+        for (int k = 0; k < c; ++k) {
+          int l = I.route_links[rb + k];
+          I.x_hi[total + off + k] = ((unsigned long long)l << 32) | (unsigned)p;
+          I.x_lo[total + off + k] = 0;
+          I.x_val[total + off + k] = want;
+        }
+        I.s_rate[p] = want;  // stash want
+      }
+      total += tot;
+    }
+    g.sync();
+    if (total > I.X_cap) {
+      fail(ERR_INTERNAL, CHK_CAP_SCRATCH);
+      return;
+    }
+    // order by (link, active position) -> demand per link in active order
+    for (int i = g.lane(); i < total; i += G::N) {
+      unsigned long long hi = I.x_hi[i];
+      unsigned p = (unsigned)(hi & 0xffffffffu);
+      I.x_lo[i] = p;
+      I.x_hi[i] = hi >> 32;
+    }
+    g.sync();
+    sort_x(total);
+    int nseg = 0;
+    for (int base = 0; base < total; base += G::N) {
+      int i = base + g.lane();
+      int h = 0;
+      if (i < total) h = (i == 0 || I.x_hi[i] != I.x_hi[i - 1]) ? 1 : 0;
+      int tot;
+      int off = g.excl_scan(h, &tot);
+      if (h) I.x_seg[nseg + off] = i;
+      nseg += tot;
+    }
+    g.sync();
+    for (int k = g.lane(); k < nseg; k += G::N) {
+      int i0 = I.x_seg[k];
+      int i1 = (k + 1 < nseg) ? I.x_seg[k + 1] : total;
+      double d = 0.0;
+      for (int i = i0; i < i1; ++i) d = dadd(d, I.x_val[i]);
+      I.l_x[(int)I.x_hi[i0]] = d;
+    }
+    g.sync();
+    for (int i = g.lane(); i < nd; i += G::N) {
+      int p = I.s_ord[i];
+      int fid = I.a_fid[p];
+      double slack = dsub(I.f_dl[fid], s.now);
+      if (!(slack > 0.0)) continue;
+      double want = I.s_rate[p];
+      double scale = 1.0;
+      int rb = rbeg(fid), rn = rlen(fid);
+      for (int k = 0; k < rn; ++k) {
+        int l = I.route_links[rb + k];
+        double c = I.cap[l];
+        double dmd = I.l_x[l];
+        if (dmd > c) scale = smin(scale, ddiv(c, dmd));
+      }
+      I.s_cap[p] = dmul(want, scale);
+    }
+    g.sync();
+  }
+
+  // ============================================ K3: strict-priority filling
+  MF_FN double residual(int l) const {
+    return I.l_stamp[l] == s.epoch ? I.l_res[l] : I.cap[l];
+  }
+  MF_FN void set_residual(int l, double v) {
+    I.l_res[l] = v;
+    I.l_stamp[l] = s.epoch;
+  }
+
+  // allocator.cpp:28-126 over the classes in s_ord/s_cls; rates -> s_rate
+  MF_NOINLINE void allocate(int ncls, bool has_caps) {
+    ++s.epoch;
+    if (s.epoch == 0) {  // stamp wrap: reset
+      for (int l = g.lane(); l < I.nlinks; l += G::N) I.l_stamp[l] = 0;
+      g.sync();
+      s.epoch = 1;
+    }
+    // rate-map insertion order for the hash emulation
+    const int A = s.n_active;
+    for (int i = g.lane(); i < A; i += G::N) {
+      int fid = I.a_fid[I.s_ord[i]];
+      I.h_keys[i] = fid;
+      I.f_hidx[fid] = i;
+    }
+    g.sync();
+    s.h_n = A;
+    s.h_ready = 0;
+    for (int c = 0; c < ncls; ++c) {
+      const int o0 = I.s_cls[c], o1 = I.s_cls[c + 1];
+      const int n = o1 - o0;
+      ++s.classes;
+      if (n == 1) {
+        const int p = I.s_ord[o0];
+        const int fid = I.a_fid[p];
+        const int rb = rbeg(fid), rn = rlen(fid);
+        double r = MF_INF;
+        if (has_caps) {
+          double cp = I.s_cap[p];
+          if (cp < MF_INF) r = smax(0.0, cp);
+        }
+        for (int k = 0; k < rn; ++k) r = smin(r, smax(0.0, residual(I.route_links[rb + k])));
+        g.sync();
+        if (g.leader()) {
+          for (int k = 0; k < rn; ++k) {
+            int l = I.route_links[rb + k];
+            set_residual(l, dsub(residual(l), r));
+          }
+          I.s_rate[p] = r;
+        }
+        g.sync();
+        s.algo_bytes += 20LL * rn + 12;
+        continue;
+      }
+      // multi-flow class: progressive filling rounds
+      for (int i = g.lane(); i < n; i += G::N) {
+        int p = I.s_ord[o0 + i];
+        I.s_rate[p] = 0.0;
+        I.s_frz[p] = 0;
+      }
+      g.sync();
+      long long guard = (long long)n + I.nlinks + 2;
+      while (guard-- > 0) {
+        ++s.rounds;
+        // count unfrozen flows per link; first toucher owns the link
+        bool any = false;
+        for (int i = g.lane(); i < n; i += G::N) {
+          int p = I.s_ord[o0 + i];
+          if (I.s_frz[p]) continue;
+          any = true;
+          int fid = I.a_fid[p];
+          int rb = rbeg(fid), rn = rlen(fid);
+          unsigned own = 0;
+          for (int k = 0; k < rn; ++k) {
+            int old = g.atomic_add(&I.l_cnt[I.route_links[rb + k]], 1);
+            if (old == 0) own |= 1u << k;
+          }
+          I.s_own[p] = (uint8_t)own;
+        }
+        g.sync();
+        if (!g.any(any)) break;
+        // inc = min over touched links and caps
+        double inc = MF_INF;
+        for (int i = g.lane(); i < n; i += G::N) {
+          int p = I.s_ord[o0 + i];
+          if (I.s_frz[p]) continue;
+          int fid = I.a_fid[p];
+          int rb = rbeg(fid), rn = rlen(fid);
+          unsigned own = I.s_own[p];
+          for (int k = 0; k < rn; ++k) {
+            if (!(own & (1u << k))) continue;
+            int l = I.route_links[rb + k];
+            inc = smin(inc, ddiv(smax(0.0, residual(l)), (double)I.l_cnt[l]));
+          }
+          if (has_caps) {
+            double cp = I.s_cap[p];
+            if (cp < MF_INF) inc = smin(inc, dsub(smax(0.0, cp), I.s_rate[p]));
+          }
+        }
+        for (int m = G::N / 2; m > 0; m >>= 1) inc = smin(inc, g.shfl_xor(inc, m));
+        inc = smax(inc, 0.0);
+        // apply
+        for (int i = g.lane(); i < n; i += G::N) {
+          int p = I.s_ord[o0 + i];
+          if (I.s_frz[p]) continue;
+          I.s_rate[p] = dadd(I.s_rate[p], inc);
+          int fid = I.a_fid[p];
+          int rb = rbeg(fid), rn = rlen(fid);
+          unsigned own = I.s_own[p];
+          for (int k = 0; k < rn; ++k) {
+            if (!(own & (1u << k))) continue;
+            int l = I.route_links[rb + k];
+            set_residual(l, dsub(residual(l), dmul(inc, (double)I.l_cnt[l])));
+          }
+        }
+        g.sync();
+        // freeze
+        bool froze = false;
+        for (int i = g.lane(); i < n; i += G::N) {
+          int p = I.s_ord[o0 + i];
+          if (I.s_frz[p]) continue;
+          double cp = MF_INF;
+          if (has_caps) {
+            double c0 = I.s_cap[p];
+            if (c0 < MF_INF) cp = smax(0.0, c0);
+          }
+          double cap_eps = dmul(1e-12, smax(1.0, cp == MF_INF ? 0.0 : cp));
+          bool stop = I.s_rate[p] >= dsub(cp, cap_eps);
+          int fid = I.a_fid[p];
+          int rb = rbeg(fid), rn = rlen(fid);
+          if (!stop) {
+            for (int k = 0; k < rn; ++k) {
+              int l = I.route_links[rb + k];
+              if (residual(l) <= dmul(1e-12, I.cap[l])) {
+                stop = true;
+                break;
+              }
+            }
+          }
+          if (stop) {
+            I.s_frz[p] = 2;  // frozen this round (counts still to reset)
+            froze = true;
+          }
+        }
+        g.sync();
+        // reset counts of the links touched this round
+        for (int i = g.lane(); i < n; i += G::N) {
+          int p = I.s_ord[o0 + i];
+          int fz = I.s_frz[p];
+          if (fz == 1) continue;
+          int fid = I.a_fid[p];
+          int rb = rbeg(fid);
+          unsigned own = I.s_own[p];
+          for (int k = 0; own; ++k, own >>= 1)
+            if (own & 1u) I.l_cnt[I.route_links[rb + k]] = 0;
+          I.s_own[p] = 0;
+          if (fz == 2) I.s_frz[p] = 1;
+        }
+        g.sync();
+        s.algo_bytes += (long long)n * (20LL * I.rmax + 29);
+        if (!g.any(froze)) {
+          fail(ERR_INTERNAL, CHK_NO_PROGRESS);
+          return;
+        }
+      }
+    }
+  }
+
+  // engine.cpp:278-293
+  MF_NOINLINE void recompute_rates() {
+    bool has_caps = false;
+    int ncls = decide(&has_caps);
+    if (s.err) return;
+    ++s.steps;
+    allocate(ncls, has_caps);
+    if (s.err) return;
+    const int A = s.n_active;
+    unsigned long long seq0 = s.seq;
+    int pushed = 0;
+    for (int base = 0; base < A; base += G::N) {
+      int p = base + g.lane();
+      int c = 0;
+      double r = 0.0;
+      bool chg = false;
+      if (p < A) {
+        r = I.s_rate[p];
+        chg = !(r == I.a_rate[p]);
+        c = (chg && r > 0.0) ? 1 : 0;
+      }
+      int tot;
+      int off = g.excl_scan(c, &tot);
+      if (chg) {
+        I.a_rate[p] = r;
+        if (r > 0.0) {
+          I.a_evt[p] = dadd(s.now, ddiv(I.a_rem[p], r));
+          I.a_evseq[p] = seq0 + (unsigned long long)(pushed + off);
+        } else {
+          I.a_evseq[p] = kNoSeq;
+        }
+      }
+      pushed += tot;
+    }
+    g.sync();
+    s.seq += (unsigned long long)pushed;
+    s.pushes += pushed;
+    s.algo_bytes += 32LL * A;
+  }
+
+  // ===================================================== K1: stage DAG
+  MF_FN bool layer_deps_met(int b, int layer) const {  // engine.cpp:356-369
+    const int base = I.b_lbase[b];
+    const int idx = layer - 1;
+    if (layer > 1) {
+      if (!I.pl_done[base + idx - 1]) return false;
+      int c = I.pl_coll[base + idx - 1];
+      if (c >= 0 && I.c_open[c] > 0) return false;
+    }
+    const int ro = I.pl_roff[base + idx], rc = I.pl_rcnt[base + idx];
+    for (int k = 0; k < rc; ++k) {
+      int fid = I.rpool[ro + k];
+      int r = I.f_req[fid];
+      if (r >= 0 && I.r_pruned[r]) continue;
+      if (!done(fid)) return false;
+    }
+    return true;
+  }
+
+  MF_FN void try_start_layers(int b) {  // engine.cpp:371-382
+    const int L = I.b_layers[b];
+    const int base = I.b_lbase[b];
+    for (int layer = 1; layer <= L; ++layer) {
+      const int idx = base + layer - 1;
+      if (I.pl_started[idx]) continue;
+      if (!layer_deps_met(b, layer)) return;
+      g.sync();
+      if (g.leader()) {
+        I.pl_started[idx] = 1;
+        I.pl_start[idx] = s.now;
+      }
+      g.sync();
+      push(dadd(s.now, I.pl_cost[idx]), EV_COMPUTE, b, layer);
+      return;
+    }
+  }
+
+  MF_FN void check_pipeline_done(int b) {  // engine.cpp:384-393
+    if (I.b_done[b] != kNoTime) return;
+    const int L = I.b_layers[b];
+    const int base = I.b_lbase[b];
+    for (int i = 0; i < L; ++i) {
+      if (!I.pl_done[base + i]) return;
+      int c = I.pl_coll[base + i];
+      if (c >= 0 && I.c_open[c] > 0) return;
+    }
+    put(&I.b_done[b], s.now);
+    push(s.now, EV_DEPART, b, -1);
+  }
+
+  MF_FN void try_complete_request(int r) {  // engine.cpp:585-593
+    if (I.r_ttft[r] != kNoTime) return;
+    const int b = I.r_batch[r];
+    if (b < 0 || I.b_done[b] == kNoTime) return;
+    if (I.r_open[r] > 0) return;
+    double t = I.b_done[b];
+    double lf = I.r_lastfin[r];
+    if (lf != kNoTime) t = smax(t, lf);
+    put(&I.r_ttft[r], t);
+  }
+
+  MF_NOINLINE void finish_flow(int fid) {  // engine.cpp:318-354
+    if (done(fid)) {
+      fail(ERR_INTERNAL, CHK_FINISHED_TWICE);
+      return;
+    }
+    const int pos = I.f_apos[fid];
+    if (pos >= 0) {
+      double rem = I.a_rem[pos];
+      if (!(rem <= dadd(dmul(1e-6, smax(I.f_size[fid], 1.0)), 1e-9))) {
+        fail(ERR_INTERNAL, CHK_EARLY_FINISH);
+        return;
+      }
+    }
+    g.sync();
+    if (g.leader()) {
+      I.f_state[fid] = FL_DONE;
+      I.f_fin[fid] = s.now;
+    }
+    g.sync();
+    remove_active(fid);
+    s.dirty = 1;
+    const int b = I.f_batch[fid];
+    if (b >= 0) put(&I.b_open[b], I.b_open[b] - 1);
+    const int c = I.f_cof[fid];
+    if (c >= 0) {
+      const int open = I.c_open[c];
+      if (!(open > 0)) {
+        fail(ERR_INTERNAL, CHK_COFLOW_BARRIER);
+        return;
+      }
+      put(&I.c_open[c], open - 1);
+      if (open - 1 == 0) {
+        put(&I.c_done[c], s.now);
+        const int cb = I.c_batch[c];
+        on_layer_boundary(cb);
+        if (s.err) return;
+        try_start_layers(cb);
+        check_pipeline_done(cb);
+      }
+    }
+    const int r = I.f_req[fid];
+    if (r >= 0) {
+      put(&I.r_open[r], I.r_open[r] - 1);
+      put(&I.r_lastfin[r], smax(I.r_lastfin[r], s.now));
+      if (I.f_stage[fid] == ST_REUSE && b >= 0) {
+        try_start_layers(b);
+        check_pipeline_done(b);
+      }
+      try_complete_request(r);
+    }
+  }
+
+  MF_NOINLINE void release_flow(int fid) {  // engine.cpp:295-316
+    if (I.f_state[fid] != FL_PENDING) {
+      fail(ERR_INTERNAL, CHK_RELEASED_TWICE);
+      return;
+    }
+    const int r = I.f_req[fid];
+    const bool pr = r >= 0 && I.r_pruned[r];
+    g.sync();
+    if (g.leader()) {
+      I.f_rel[fid] = s.now;
+      I.f_state[fid] = pr ? FL_PRUNED : FL_ACTIVE;
+    }
+    g.sync();
+    on_flow_released(fid);
+    if (s.err) return;
+    const int c = I.f_cof[fid];
+    if (c >= 0 && I.c_rel[c] == kNoTime) put(&I.c_rel[c], s.now);
+    if (I.f_size[fid] <= 0.0 || rlen(fid) == 0) {
+      finish_flow(fid);
+      return;
+    }
+    if (s.n_active >= I.A_cap) {
+      fail(ERR_INTERNAL, CHK_CAP_ACTIVE);
+      return;
+    }
+    const int pos = s.n_active;
+    g.sync();
+    if (g.leader()) {
+      I.a_fid[pos] = fid;
+      I.a_rem[pos] = I.f_size[fid];
+      I.a_rate[pos] = 0.0;
+      I.a_evt[pos] = 0.0;
+      I.a_evseq[pos] = kNoSeq;
+      I.f_apos[fid] = pos;
+    }
+    g.sync();
+    ++s.n_active;
+    if (s.n_active > s.max_active) s.max_active = s.n_active;
+    s.dirty = 1;
+  }
+
+  MF_NOINLINE void handle_compute_complete(int b, int layer) {  // engine.cpp:395-418
+    const int idx = I.b_lbase[b] + layer - 1;
+    if (!(I.pl_started[idx] && !I.pl_done[idx])) {
+      fail(ERR_INTERNAL, CHK_COMPUTE_STATE);
+      return;
+    }
+    if (!layer_deps_met(b, layer)) {
+      fail(ERR_INTERNAL, CHK_LAYER_DEPS);
+      return;
+    }
+    g.sync();
+    if (g.leader()) {
+      I.pl_done[idx] = 1;
+      I.pl_end[idx] = s.now;
+    }
+    g.sync();
+    on_layer_boundary(b);
+    if (s.err) return;
+    const int c = I.pl_coll[idx];
+    if (c >= 0) {
+      const int mo = I.c_moff[c], mc = I.c_mcnt[c];
+      for (int k = 0; k < mc; ++k) {
+        int fid = I.cpool[mo + k];
+        if (!(I.f_scripted[fid] & 1) && I.f_state[fid] == FL_PENDING) release_flow(fid);
+        if (s.err) return;
+      }
+    }
+    const int po = I.pl_poff[idx], pc = I.pl_pcnt[idx];
+    for (int k = 0; k < pc; ++k) {
+      int fid = I.ppool[po + k];
+      if (!(I.f_scripted[fid] & 1) && I.f_state[fid] == FL_PENDING) release_flow(fid);
+      if (s.err) return;
+    }
+    try_start_layers(b);
+    check_pipeline_done(b);
+    s.dirty = 1;
+  }
+
+  MF_FN bool p2d_left(int b) {
+    const int f0 = I.b_ffirst[b], fc = I.b_fcount[b];
+    bool left = false;
+    for (int i = g.lane(); i < fc; i += G::N) {
+      int fid = f0 + i;
+      if (I.f_stage[fid] == ST_P2D && !done(fid)) left = true;
+    }
+    return g.any(left);
+  }
+
+  MF_NOINLINE void handle_batch_depart(int b) {  // engine.cpp:420-438
+    if (I.b_departed[b]) return;
+    put(&I.b_departed[b], (uint8_t)1);
+    if (I.p.workload_mode) {
+      put(&I.u_busy[I.b_unit[b]], (uint8_t)0);
+      push(s.now, EV_ADMIT, I.b_unit[b], -1);
+    }
+    if (p2d_left(b) && I.p.policy == POL_MFS) push(dadd(s.now, I.p.tick), EV_TICK, b, -1);
+    batch_event_hook();
+    if (s.err) return;
+    const int mo = I.b_moff[b], mc = I.b_mcnt[b];
+    for (int k = 0; k < mc; ++k) try_complete_request(I.m_pool[mo + k]);
+    s.dirty = 1;
+  }
+
+  // register one flow; ids are registration order (engine.cpp:122-137)
+  MF_FN int register_flow(int req, int b, int stage, int route, double size, int tl, double dl) {
+    if (s.n_flows >= I.F_cap) {
+      fail(ERR_INTERNAL, CHK_CAP_FLOWS);
+      return -1;
+    }
+    const int fid = s.n_flows++;
+    if (g.leader()) {
+      I.f_size[fid] = size;
+      I.f_rel[fid] = kNoTime;
+      I.f_fin[fid] = kNoTime;
+      I.f_dl[fid] = dl;
+      I.f_req[fid] = req;
+      I.f_batch[fid] = b;
+      I.f_cof[fid] = -1;
+      I.f_route[fid] = route;
+      I.f_apos[fid] = -1;
+      I.f_rank[fid] = 0;
+      I.f_tl[fid] = tl;
+      I.f_hidx[fid] = -1;
+      I.f_stage[fid] = (uint8_t)stage;
+      I.f_state[fid] = FL_PENDING;
+      I.f_band[fid] = BD_EARLY;
+      I.f_level[fid] = 1;
+      I.f_scripted[fid] = 0;
+      if (req >= 0) I.r_open[req] += 1;
+    }
+    return fid;
+  }
+
+  MF_NOINLINE void admit_batch(int unit, int moff, int mcnt) {  // engine.cpp:455-533
+    if (mcnt <= 0) {
+      fail(ERR_INTERNAL, CHK_EMPTY_BATCH);
+      return;
+    }
+    if (s.n_batches >= I.B_cap) {
+      fail(ERR_INTERNAL, CHK_CAP_BATCHES);
+      return;
+    }
+    const int b = s.n_batches++;
+    const int L = I.p.layers;
+    const int lbase = b * L;
+    double batch_tokens = 0.0;
+    for (int k = 0; k < mcnt; ++k)
+      batch_tokens = dadd(batch_tokens, (double)I.r_tokens[I.m_pool[moff + k]]);
+    const double cost = dadd(I.p.alpha, dmul(I.p.beta, batch_tokens));
+    g.sync();
+    if (g.leader()) {
+      I.b_unit[b] = unit;
+      I.b_layers[b] = L;
+      I.b_lbase[b] = lbase;
+      I.b_admit[b] = s.now;
+      I.b_done[b] = kNoTime;
+      I.b_departed[b] = 0;
+      I.b_admitted[b] = 1;
+      I.b_open[b] = 0;
+      I.b_rank[b] = -1;
+      I.b_ffirst[b] = s.n_flows;
+      I.b_fcount[b] = 0;
+      I.b_moff[b] = moff;
+      I.b_mcnt[b] = mcnt;
+      for (int k = 0; k < mcnt; ++k) I.r_batch[I.m_pool[moff + k]] = b;
+    }
+    // per-layer pipeline records
+    if (s.rp_top + L * mcnt > I.RP_cap || s.pp_top + L * mcnt > I.PP_cap) {
+      fail(ERR_INTERNAL, CHK_CAP_POOL);
+      return;
+    }
+    for (int i = g.lane(); i < L; i += G::N) {
+      int idx = lbase + i;
+      I.pl_cost[idx] = cost;
+      I.pl_started[idx] = 0;
+      I.pl_done[idx] = 0;
+      I.pl_start[idx] = kNoTime;
+      I.pl_end[idx] = kNoTime;
+      I.pl_coll[idx] = -1;
+      I.pl_roff[idx] = s.rp_top + i * mcnt;
+      I.pl_rcnt[idx] = 0;
+      I.pl_poff[idx] = s.pp_top + i * mcnt;
+      I.pl_pcnt[idx] = 0;
+    }
+    g.sync();
+    s.rp_top += L * mcnt;
+    s.pp_top += L * mcnt;
+    const int first = s.n_flows;
+    // request-owned flows (build_msflows, engine.cpp:49-89)
+    const double kv = I.p.kv;
+    for (int k = 0; k < mcnt; ++k) {
+      const int r = I.m_pool[moff + k];
+      const double tokens = (double)I.r_tokens[r];
+      const int u = I.r_unit[r];
+      const int lc = I.r_layers[r];
+      const double reuse_bytes = dmul(dmul(I.r_reuse[r], tokens), kv);
+      const double p2d_bytes = dmul(tokens, kv);
+      if (reuse_bytes > 0.0 && I.r_src[r] < 0) {
+        fail(ERR_WORKLOAD, CHK_REUSE_SOURCE);
+        return;
+      }
+      const double dl = I.r_deadline[r];
+      const int rr = reuse_bytes > 0.0 ? I.rt_reuse[I.r_src[r] * I.p.units + u] : -1;
+      const int rp = I.rt_p2d[u];
+      if (s.n_flows + 2 * lc > I.F_cap) {
+        fail(ERR_INTERNAL, CHK_CAP_FLOWS);
+        return;
+      }
+      for (int l = 1; l <= lc; ++l) {
+        const int idx = lbase + l - 1;
+        if (reuse_bytes > 0.0) {
+          int fid = register_flow(r, b, ST_REUSE, rr, reuse_bytes, l, NAN);
+          if (g.leader()) {
+            int n = I.pl_rcnt[idx];
+            I.rpool[I.pl_roff[idx] + n] = fid;
+            I.pl_rcnt[idx] = n + 1;
+          }
+        }
+        if (p2d_bytes > 0.0) {
+          int fid = register_flow(r, b, ST_P2D, rp, p2d_bytes, l, dl);
+          if (g.leader()) {
+            int n = I.pl_pcnt[idx];
+            I.ppool[I.pl_poff[idx] + n] = fid;
+            I.pl_pcnt[idx] = n + 1;
+          }
+        }
+      }
+      g.sync();
+    }
+    // batch-owned collectives: all-to-all among the unit's hosts
+    const double coll_bytes = dmul(batch_tokens, I.p.coll);
+    const int h = I.p.hpu;
+    if (coll_bytes > 0.0 && h > 1) {
+      const int per = h * (h - 1);
+      if (s.n_flows + L * per > I.F_cap) {
+        fail(ERR_INTERNAL, CHK_CAP_FLOWS);
+        return;
+      }
+      if (s.n_coflows + L > I.C_cap || s.cm_top + L * per > I.CM_cap) {
+        fail(ERR_INTERNAL, CHK_CAP_COFLOWS);
+        return;
+      }
+      for (int l = 1; l <= L; ++l) {
+        const int c = s.n_coflows++;
+        const int f0 = s.n_flows;
+        for (int t = g.lane(); t < per; t += G::N) {
+          int i = t / (h - 1);
+          int j = t % (h - 1);
+          if (j >= i) ++j;
+          int fid = f0 + t;
+          I.f_size[fid] = coll_bytes;
+          I.f_rel[fid] = kNoTime;
+          I.f_fin[fid] = kNoTime;
+          I.f_dl[fid] = NAN;
+          I.f_req[fid] = -1;
+          I.f_batch[fid] = b;
+          I.f_cof[fid] = c;
+          I.f_route[fid] = I.rt_coll[(unit * h + i) * h + j];
+          I.f_apos[fid] = -1;
+          I.f_rank[fid] = 0;
+          I.f_tl[fid] = l;
+          I.f_hidx[fid] = -1;
+          I.f_stage[fid] = ST_COLL;
+          I.f_state[fid] = FL_PENDING;
+          I.f_band[fid] = BD_EARLY;
+          I.f_level[fid] = 1;
+          I.f_scripted[fid] = 0;
+          I.cpool[s.cm_top + t] = fid;
+        }
+        g.sync();
+        if (g.leader()) {
+          I.c_batch[c] = b;
+          I.c_layer[c] = l;
+          I.c_open[c] = per;
+          I.c_rel[c] = kNoTime;
+          I.c_done[c] = kNoTime;
+          I.c_moff[c] = s.cm_top;
+          I.c_mcnt[c] = per;
+          I.pl_coll[lbase + l - 1] = c;
+        }
+        g.sync();
+        s.n_flows += per;
+        s.cm_top += per;
+      }
+    }
+    const int nf = s.n_flows - first;
+    g.sync();
+    if (g.leader()) {
+      I.b_fcount[b] = nf;
+      I.b_open[b] = nf;
+    }
+    g.sync();
+    live_append(b);
+    // reuse launches at admission, in (member, layer) order
+    for (int k = 0; k < mcnt; ++k) {
+      const int r = I.m_pool[moff + k];
+      const int lc = I.r_layers[r];
+      for (int l = 1; l <= lc; ++l) {
+        const int idx = lbase + l - 1;
+        const int ro = I.pl_roff[idx], rc = I.pl_rcnt[idx];
+        for (int q = 0; q < rc; ++q) {
+          int fid = I.rpool[ro + q];
+          if (I.f_req[fid] == r && I.f_state[fid] == FL_PENDING) {
+            release_flow(fid);
+            if (s.err) return;
+          }
+        }
+      }
+    }
+    put(&I.u_busy[unit], (uint8_t)1);
+    try_start_layers(b);
+    check_pipeline_done(b);
+    batch_event_hook();
+    s.dirty = 1;
+  }
+
+  MF_FN void handle_admit_try(int unit) {  // engine.cpp:440-453
+    if (I.u_busy[unit]) return;
+    const int head = I.q_head[unit], tail = I.q_tail[unit];
+    if (head == tail) return;
+    const int qo = I.q_off[unit];
+    int cnt = 0;
+    long long tokens = 0;
+    while (head + cnt < tail) {
+      const int r = I.m_pool[qo + head + cnt];
+      const long long t = I.r_tokens[r];
+      if (cnt > 0 && tokens + t > I.p.max_batch_tokens) break;
+      ++cnt;
+      tokens += t;
+    }
+    put(&I.q_head[unit], head + cnt);
+    admit_batch(unit, qo + head, cnt);
+  }
+
+  MF_NOINLINE void activate_manual_batch(int b) {  // engine.cpp:541-558
+    if (I.b_admitted[b]) return;
+    put(&I.b_admitted[b], (uint8_t)1);
+    const int f0 = I.b_ffirst[b], fc = I.b_fcount[b];
+    for (int i = 0; i < fc; ++i) {
+      const int fid = f0 + i;
+      if (I.f_scripted[fid] & 1) {
+        push(smax(s.now, I.f_relat[fid]), EV_RELEASE, fid, -1);
+      } else if (I.f_stage[fid] == ST_REUSE) {
+        release_flow(fid);
+      }
+      if (s.err) return;
+    }
+    try_start_layers(b);
+    check_pipeline_done(b);
+    batch_event_hook();
+    s.dirty = 1;
+  }
+
+  MF_FN void live_append(int b) {
+    if (s.n_live >= I.B_cap) {
+      fail(ERR_INTERNAL, CHK_CAP_BATCHES);
+      return;
+    }
+    put(&I.g_batches[s.n_live], b);
+    ++s.n_live;
+  }
+
+  // =============================================== K5: MFS Algorithm 1
+  MF_NOINLINE void batch_event_hook() {  // engine.cpp:560-583
+    if (I.p.policy != POL_MFS) return;
+    int np = on_batch_event();
+    if (s.err || np == 0) return;
+    // apply_prunes, ascending request id
+    for (int k = 0; k < np; ++k) {
+      const int r = I.g_pruned[k];
+      put(&I.r_pruned[r], (uint8_t)1);
+      const int b = I.r_batch[r];
+      if (b < 0) continue;
+      const int f0 = I.b_ffirst[b], fc = I.b_fcount[b];
+      for (int i = g.lane(); i < fc; i += G::N) {
+        int fid = f0 + i;
+        if (I.f_req[fid] != r || I.f_state[fid] == FL_DONE) continue;
+        I.f_band[fid] = BD_SCAV;
+        if (I.f_state[fid] == FL_ACTIVE) I.f_state[fid] = FL_PRUNED;
+      }
+      g.sync();
+      try_start_layers(b);
+      check_pipeline_done(b);
+    }
+    s.pruned += np;
+    s.dirty = 1;
+  }
+
+  // request load on one link from its sparse vector
+  MF_FN double req_load(int j, int l) const {
+    const int o = I.g_loff[j], n = I.g_lcnt[j];
+    for (int k = 0; k < n; ++k)
+      if (I.g_link[o + k] == l) return I.g_load[o + k];
+    return 0.0;
+  }
+
+  // est_finish_time (inter_request.cpp:53-78) over the dense S (l_x) + L (l_y)
+  MF_FN double est_finish(double comp, int* u_star) {
+    double worst = 0.0;
+    int ustar = 0;
+    for (int u = g.lane(); u < I.nlinks; u += G::N) {
+      double total = dadd(I.l_x[u], I.l_y[u]);
+      double ratio = ddiv(total, I.cap[u]);
+      if (ratio > worst) {
+        worst = ratio;
+        ustar = u;
+      }
+    }
+    for (int m = G::N / 2; m > 0; m >>= 1) {
+      double ow = g.shfl_xor(worst, m);
+      int ou = g.shfl_xor(ustar, m);
+      if (ow > worst || (ow == worst && ou < ustar)) {
+        worst = ow;
+        ustar = ou;
+      }
+    }
+    if (worst == 0.0) ustar = 0;
+    *u_star = ustar;
+    return worst == MF_INF ? MF_INF : dadd(dadd(s.now, comp), worst);
+  }
+
+  // rmlq.cpp:268-382 + inter_scheduling (inter_request.cpp:90-164).
+  // Returns the number of newly pruned requests (ascending, in g_pruned).
+  MF_NOINLINE int on_batch_event() {
+    // live (undrained) batches, creation order; drained is permanent
+    int nl = 0;
+    for (int base = 0; base < s.n_live; base += G::N) {
+      int i = base + g.lane();
+      int b = -1, c = 0;
+      if (i < s.n_live) {
+        b = I.g_batches[i];
+        c = batch_drained(b) ? 0 : 1;
+      }
+      int tot;
+      int off = g.excl_scan(c, &tot);
+      g.sync();
+      if (c) I.g_batches[nl + off] = b;
+      nl += tot;
+      g.sync();
+    }
+    s.n_live = nl;
+    // in-flight unpruned requests, batch-major (slot = live batch with any)
+    int nreq = 0, nb = 0;
+    for (int i = 0; i < nl; ++i) {
+      const int b = I.g_batches[i];
+      const int mo = I.b_moff[b], mc = I.b_mcnt[b];
+      int cnt = 0;
+      double toks = 0.0;
+      for (int k = 0; k < mc; ++k) {  // batch_tokens in member order
+        int r = I.m_pool[mo + k];
+        if (!I.r_pruned[r]) toks = dadd(toks, (double)I.r_tokens[r]);
+      }
+      for (int base = 0; base < mc; base += G::N) {
+        int k = base + g.lane();
+        int c = 0, r = -1;
+        if (k < mc) {
+          r = I.m_pool[mo + k];
+          c = I.r_pruned[r] ? 0 : 1;
+        }
+        int tot;
+        int off = g.excl_scan(c, &tot);
+        if (c) {
+          I.g_req[nreq + cnt + off] = r;
+          I.g_rbat[nreq + cnt + off] = nb;
+          I.g_inpool[nreq + cnt + off] = 0;
+        }
+        cnt += tot;
+      }
+      g.sync();
+      if (cnt > 0) {
+        if (g.leader()) {
+          I.g_slot_b[nb] = b;
+          I.g_slot_off[nb] = nreq;
+          I.g_slot_cnt[nb] = cnt;
+          I.g_tok[nb] = toks;
+        }
+        g.sync();
+        ++nb;
+      }
+      nreq += cnt;
+    }
+    if (nb == 0) return 0;
+    const long long in_flight = nreq;
+    // per-request sparse loads (fold order: the batch's flows in id order)
+    bool overflow = false;
+    for (int j = g.lane(); j < nreq; j += G::N) {
+      const int r = I.g_req[j];
+      const int q = I.g_rbat[j];
+      const int b = I.g_slot_b[q];
+      const double toks = I.g_tok[q];
+      const int o = j * I.LR_cap;
+      int n = 0;
+      const int f0 = I.b_ffirst[b], fc = I.b_fcount[b];
+      for (int i = 0; i < fc && !overflow; ++i) {
+        const int fid = f0 + i;
+        if (done(fid)) continue;
+        const double rem = remaining(fid);
+        if (rem <= 0.0) continue;
+        const int rn = rlen(fid);
+        if (rn == 0) continue;
+        double add;
+        if (I.f_stage[fid] == ST_COLL) {
+          if (toks <= 0.0) continue;
+          add = ddiv(dmul(rem, (double)I.r_tokens[r]), toks);
+        } else if (I.f_req[fid] == r) {
+          add = rem;
+        } else {
+          continue;
+        }
+        const int rb = rbeg(fid);
+        for (int k = 0; k < rn; ++k) {
+          const int l = I.route_links[rb + k];
+          int e = 0;
+          while (e < n && I.g_link[o + e] != l) ++e;
+          if (e == n) {
+            if (n >= I.LR_cap) {
+              overflow = true;
+              break;
+            }
+            I.g_link[o + n] = l;
+            I.g_load[o + n] = 0.0;
+            ++n;
+          }
+          I.g_load[o + e] = dadd(I.g_load[o + e], add);
+        }
+      }
+      I.g_loff[j] = o;
+      I.g_lcnt[j] = n;
+    }
+    g.sync();
+    if (g.any(overflow)) {
+      fail(ERR_INTERNAL, CHK_CAP_SCRATCH);
+      return 0;
+    }
+    // RED score per slot (inter_request.cpp:7-43) over sorted deadlines
+    for (int q = g.lane(); q < nb; q += G::N) {
+      const int o = I.g_slot_off[q], n = I.g_slot_cnt[q];
+      for (int k = 0; k < n; ++k) {
+        double d = I.r_deadline[I.g_req[o + k]];
+        int m = k;
+        while (m > 0 && I.g_tmp[o + m - 1] > d) {
+          I.g_tmp[o + m] = I.g_tmp[o + m - 1];
+          --m;
+        }
+        I.g_tmp[o + m] = d;
+      }
+      double red, dlo;
+      const double d0 = I.g_tmp[o], dn = I.g_tmp[o + n - 1];
+      if (n == 1 || d0 == dn) {
+        red = d0;
+        dlo = d0;
+      } else {
+        int ks = 1;
+        double best = dsub(I.g_tmp[o + 1], I.g_tmp[o]);
+        for (int k = 2; k < n; ++k) {
+          double gap = dsub(I.g_tmp[o + k], I.g_tmp[o + k - 1]);
+          if (gap > best) {
+            best = gap;
+            ks = k;
+          }
+        }
+        double f = ddiv((double)ks, (double)n);
+        dlo = I.g_tmp[o + ks];
+        red = dadd(dmul(f, d0), dmul(dsub(1.0, f), dlo));
+      }
+      I.g_red[q] = red;
+      I.g_dlo[q] = dlo;
+      const int b = I.g_slot_b[q];
+      I.g_sig[q] = q;
+      I.g_sk0[q] = dord(red);
+      I.g_sk1[q] = dord(I.b_admit[b]);
+      I.g_sk2[q] = (unsigned long long)b;
+    }
+    g.sync();
+    sort_slots(nb);  // sigma: (red, admit, id)
+    for (int u = g.lane(); u < I.nlinks; u += G::N) I.l_x[u] = 0.0;
+    g.sync();
+    const long long budget =
+        I.p.prune_enable ? (long long)ceil(dmul(I.p.drop_frac, (double)in_flight)) : 0;
+    const long long drop_budget = budget > 0 ? budget : 0;
+    int npruned = 0;
+    for (int k = 0; k < nb; ++k) {
+      const int q = I.g_sig[k];
+      const int b = I.g_slot_b[q];
+      const int o = I.g_slot_off[q], n = I.g_slot_cnt[q];
+      for (int u = g.lane(); u < I.nlinks; u += G::N) I.l_y[u] = 0.0;
+      g.sync();
+      for (int jj = 0; jj < n; ++jj) {  // L += r.load in request order
+        const int j = o + jj;
+        const int lo = I.g_loff[j], ln = I.g_lcnt[j];
+        for (int e = g.lane(); e < ln; e += G::N) {
+          int l = I.g_link[lo + e];
+          I.l_y[l] = dadd(I.l_y[l], I.g_load[lo + e]);
+        }
+        if (g.leader()) {
+          I.g_inpool[j] = 1;
+          I.g_rpos[j] = k;
+        }
+        g.sync();
+      }
+      const double comp = remaining_compute(b);
+      int ustar = 0;
+      double fhat = est_finish(comp, &ustar);
+      const double dlo = I.g_dlo[q];
+      while (fhat > dlo && npruned < drop_budget) {
+        // victim: max load on u*, ties -> lowest request id
+        double vload = 0.0;
+        int vj = -1, vid = 0x7fffffff;
+        for (int j = g.lane(); j < nreq; j += G::N) {
+          if (I.g_inpool[j] != 1) continue;
+          double l = req_load(j, ustar);
+          if (l <= 0.0) continue;
+          int id = I.g_req[j];
+          if (vj < 0 || l > vload || (l == vload && id < vid)) {
+            vj = j;
+            vload = l;
+            vid = id;
+          }
+        }
+        for (int m = G::N / 2; m > 0; m >>= 1) {
+          double ol = g.shfl_xor(vload, m);
+          int oj = g.shfl_xor(vj, m);
+          int oi = g.shfl_xor(vid, m);
+          if (oj >= 0 && (vj < 0 || ol > vload || (ol == vload && oi < vid))) {
+            vj = oj;
+            vload = ol;
+            vid = oi;
+          }
+        }
+        if (vj < 0) break;  // nobody loads the bottleneck: no progress
+        put(&I.g_inpool[vj], (uint8_t)2);
+        put(&I.g_pruned[npruned], vid);
+        ++npruned;
+        double* target = (I.g_rpos[vj] == k) ? I.l_y : I.l_x;
+        const int lo = I.g_loff[vj], ln = I.g_lcnt[vj];
+        for (int e = g.lane(); e < ln; e += G::N) {
+          int l = I.g_link[lo + e];
+          target[l] = smax(0.0, dsub(target[l], I.g_load[lo + e]));
+        }
+        g.sync();
+        fhat = est_finish(comp, &ustar);
+      }
+      for (int u = g.lane(); u < I.nlinks; u += G::N) I.l_x[u] = dadd(I.l_x[u], I.l_y[u]);
+      g.sync();
+    }
+    // ranks from sigma (rmlq.cpp:355-360): every member, pruned or not
+    for (int k = 0; k < nb; ++k) {
+      const int b = I.g_slot_b[I.g_sig[k]];
+      const int mo = I.b_moff[b], mc = I.b_mcnt[b];
+      for (int i = g.lane(); i < mc; i += G::N) I.r_rank[I.m_pool[mo + i]] = k + 1;
+      if (g.leader()) I.b_rank[b] = k + 1;
+      g.sync();
+    }
+    // rerank not-done flows of every live batch (rmlq.cpp:364-373)
+    for (int i = 0; i < nl; ++i) {
+      const int b = I.g_batches[i];
+      const int f0 = I.b_ffirst[b], fc = I.b_fcount[b];
+      for (int t = g.lane(); t < fc; t += G::N) {
+        int fid = f0 + t;
+        if (!done(fid)) I.f_rank[fid] = rank_of(fid);
+      }
+      g.sync();
+    }
+    if (g.leader()) {  // pruned ids ascending (inter_request.cpp:162)
+      for (int a = 1; a < npruned; ++a) {
+        int v = I.g_pruned[a];
+        int m = a;
+        while (m > 0 && I.g_pruned[m - 1] > v) {
+          I.g_pruned[m] = I.g_pruned[m - 1];
+          --m;
+        }
+        I.g_pruned[m] = v;
+      }
+    }
+    g.sync();
+    s.algo_bytes += 64LL * nreq + 16LL * I.nlinks * nb;
+    return npruned;
+  }
+
+  // sort sigma slots g_sig by (g_sk0, g_sk1, g_sk2)
+  MF_FN bool slot_less(int a, int b) const {
+    if (b < 0) return a >= 0;
+    if (a < 0) return false;
+    if (I.g_sk0[a] != I.g_sk0[b]) return I.g_sk0[a] < I.g_sk0[b];
+    if (I.g_sk1[a] != I.g_sk1[b]) return I.g_sk1[a] < I.g_sk1[b];
+    return I.g_sk2[a] < I.g_sk2[b];
+  }
+  MF_FN void sort_slots(int n) {
+    if (n <= 1) return;
+    const int n2 = pow2ceil(n);
+    for (int i = n + g.lane(); i < n2; i += G::N) I.g_sig[i] = -1;
+    g.sync();
+    for (int k = 2; k <= n2; k <<= 1) {
+      for (int j = k >> 1; j > 0; j >>= 1) {
+        for (int i = g.lane(); i < n2; i += G::N) {
+          int ixj = i ^ j;
+          if (ixj > i) {
+            int a = I.g_sig[i], b = I.g_sig[ixj];
+            bool up = (i & k) == 0;
+            if (up ? slot_less(b, a) : slot_less(a, b)) {
+              I.g_sig[i] = b;
+              I.g_sig[ixj] = a;
+            }
+          }
+        }
+        g.sync();
+      }
+    }
+  }
+
+  // ======================================================= main loop
+  MF_FN void init_state() {
+    // workload-mode state (manual mode arrives prepared by the host)
+    for (int r = g.lane(); r < I.n_req; r += G::N) {
+      I.r_batch[r] = -1;
+      I.r_pruned[r] = 0;
+      I.r_ttft[r] = kNoTime;
+      I.r_open[r] = 0;
+      I.r_lastfin[r] = kNoTime;
+      I.r_rank[r] = -1;
+    }
+    for (int u = g.lane(); u < I.p.units; u += G::N) {
+      I.u_busy[u] = 0;
+      I.q_head[u] = 0;
+      I.q_tail[u] = 0;
+    }
+    for (int l = g.lane(); l < I.nlinks; l += G::N) {
+      I.l_stamp[l] = 0;
+      I.l_cnt[l] = 0;
+    }
+    g.sync();
+  }
+
+  MF_NOINLINE void run() {
+    const long long seq0 = I.seq0;
+    const int n_ev0 = I.n_ev0, n_flows0 = I.n_flows0, n_batches0 = I.n_batches0,
+              n_coflows0 = I.n_coflows0;
+    s.now = 0.0;
+    s.prev_t = -1.0;
+    s.seq = (unsigned long long)seq0;
+    s.events = s.steps = s.streak = s.pushes = s.algo_bytes = s.classes = s.rounds = 0;
+    s.n_flows = n_flows0;
+    s.n_batches = n_batches0;
+    s.n_coflows = n_coflows0;
+    s.n_active = 0;
+    s.n_ev = n_ev0;
+    s.rp_top = s.pp_top = s.cm_top = 0;
+    s.next_arr = 0;
+    s.epoch = 0;
+    s.n_live = 0;
+    s.h_n = 0;
+    s.h_ready = 0;
+    s.dirty = 0;
+    s.err = 0;
+    s.chk = 0;
+    s.pruned = 0;
+    s.max_active = 0;
+    s.horizon = I.p.horizon;
+    if (!I.host_init) {
+      init_state();
+    } else {
+      for (int l = g.lane(); l < I.nlinks; l += G::N) {
+        I.l_stamp[l] = 0;
+        I.l_cnt[l] = 0;
+      }
+      g.sync();
+      for (int r = g.lane(); r < I.n_req; r += G::N) I.r_ttft[r] = kNoTime;
+      g.sync();
+      for (int b = 0; b < n_batches0; ++b) live_append(b);
+    }
+    recompute_rates();
+    s.dirty = 0;
+    while (!s.err) {
+      Ev e = next_event();
+      if (e.src == 0) break;
+      if (e.t > s.horizon) break;
+      int kind, a, b;
+      if (e.src == 1) {
+        kind = EV_ARRIVAL;
+        a = e.idx;
+        b = -1;
+        ++s.next_arr;
+      } else if (e.src == 2) {
+        kind = I.e_kind[e.idx];
+        a = I.e_a[e.idx];
+        b = I.e_b[e.idx];
+        pool_remove(e.idx);
+      } else {
+        kind = EV_FLOW;
+        a = I.a_fid[e.idx];
+        b = -1;
+      }
+      advance_to(e.t);
+      if (s.err) break;
+      ++s.events;
+      if (e.t == s.prev_t) {
+        if (++s.streak > I.p.livelock) {
+          fail(ERR_SIM, CHK_LIVELOCK);
+          break;
+        }
+      } else {
+        s.streak = 0;
+        s.prev_t = e.t;
+      }
+      switch (kind) {
+        case EV_FLOW:
+          finish_flow(a);
+          break;
+        case EV_COMPUTE:
+          handle_compute_complete(a, b);
+          break;
+        case EV_DEPART:
+          handle_batch_depart(a);
+          break;
+        case EV_ARRIVAL: {
+          const int u = I.r_unit[a];
+          put(&I.q_tail[u], I.q_tail[u] + 1);
+          push(s.now, EV_ADMIT, u, -1);
+          break;
+        }
+        case EV_ADMIT:
+          if (I.p.workload_mode)
+            handle_admit_try(a);
+          else
+            activate_manual_batch(a);
+          break;
+        case EV_RELEASE:
+          if (I.f_state[a] == FL_PENDING) release_flow(a);
+          break;
+        case EV_TICK: {
+          if (p2d_left(a)) {
+            if (promote_batch(a, true)) s.dirty = 1;
+            push(dadd(s.now, I.p.tick), EV_TICK, a, -1);
+          }
+          break;
+        }
+        default:
+          break;
+      }
+      if (s.err) break;
+      if (s.dirty) {
+        recompute_rates();
+        s.dirty = 0;
+      }
+    }
+    if (!s.err) finalize();
+    if (g.leader()) {
+      I.out[OUT_STATUS] = s.err;
+      I.out[OUT_CHECK] = s.chk;
+      I.out[OUT_EVENTS] = s.events;
+      I.out[OUT_STEPS] = s.steps;
+      I.out[OUT_NFLOWS] = s.n_flows;
+      I.out[OUT_NBATCHES] = s.n_batches;
+      I.out[OUT_NCOFLOWS] = s.n_coflows;
+      I.out[OUT_PRUNED] = s.pruned;
+      I.out[OUT_MAXACTIVE] = s.max_active;
+      I.out[OUT_PUSHES] = s.pushes;
+      I.out[OUT_ALGO_BYTES] = s.algo_bytes;
+      I.out[OUT_NOW_BITS] = (long long)dbits(s.now);
+      I.out[OUT_CLASSES] = s.classes;
+      I.out[OUT_ROUNDS] = s.rounds;
+    }
+    g.sync();
+  }
+
+  // engine.cpp:659-707: per-coflow stall and per-batch stall (coflow id order)
+  MF_NOINLINE void finalize() {
+    for (int c = g.lane(); c < s.n_coflows; c += G::N) {
+      double stall = 0.0;
+      const double dn = I.c_done[c];
+      if (dn != kNoTime) {
+        const int b = I.c_batch[c];
+        const int layer = I.c_layer[c];
+        const int base = I.b_lbase[b];
+        double other = I.pl_end[base + layer - 1];
+        if (layer < I.b_layers[b]) {
+          const int idx = base + layer;  // reuse deps of layer + 1
+          const int ro = I.pl_roff[idx], rc = I.pl_rcnt[idx];
+          for (int k = 0; k < rc; ++k) {
+            int fid = I.rpool[ro + k];
+            int r = I.f_req[fid];
+            if (r >= 0 && I.r_pruned[r]) continue;
+            double fin = I.f_fin[fid];
+            if (fin != kNoTime) other = smax(other, fin);
+          }
+        }
+        stall = smax(0.0, dsub(dn, other));
+      }
+      I.c_stall[c] = stall;
+    }
+    g.sync();
+    for (int b = g.lane(); b < s.n_batches; b += G::N) {
+      const int L = I.b_layers[b];
+      const int base = I.b_lbase[b];
+      double sum = 0.0;
+      int last = -1;
+      for (int t = 0; t < L; ++t) {
+        int nxt = 0x7fffffff;
+        for (int l = 0; l < L; ++l) {
+          int c = I.pl_coll[base + l];
+          if (c > last && c < nxt) nxt = c;
+        }
+        if (nxt == 0x7fffffff) break;
+        sum = dadd(sum, I.c_stall[nxt]);
+        last = nxt;
+      }
+      I.b_stall[b] = sum;
+    }
+    g.sync();
+    for (int r = g.lane(); r < I.n_req; r += G::N) {
+      const int b = I.r_batch[r];
+      I.r_stall[r] = b >= 0 ? I.b_stall[b] : 0.0;
+      I.o_pruned[r] = I.r_pruned[r];
+      I.o_rbatch[r] = b;
+    }
+    g.sync();
+  }
+};
+
+}  // namespace mfb

@@ -1,0 +1,102 @@
+// Lane-group abstraction for the warp-per-instance engine.
+//
+// The engine is written once as warp-synchronous code: scalar control flow is
+// executed uniformly by every lane of the group (all lanes hold identical
+// register copies of scalar state), data-parallel loops stride over lanes, and
+// every store to shared instance state in a scalar section goes through
+// G::put (one writer, fenced by __syncwarp on both sides).
+//
+//   WarpLanes   -- the product: one 32-lane warp on sm_100a owns one instance.
+//   SerialLanes -- a 1-lane host build of the SAME engine source, used only by
+//                  the CPU test tier to debug engine logic without a GPU. It is
+//                  never linked into the product library.
+#pragma once
+#include <stdint.h>
+
+#if defined(__CUDACC__)
+#define MF_FN __device__ __forceinline__
+#define MF_NOINLINE __device__ __noinline__
+#else
+#define MF_FN inline
+#define MF_NOINLINE
+#endif
+
+namespace mfb {
+
+#if defined(__CUDACC__)
+struct WarpLanes {
+  static constexpr int N = 32;
+  MF_FN int lane() const { return threadIdx.x & 31; }
+  MF_FN bool leader() const { return (threadIdx.x & 31) == 0; }
+  MF_FN void sync() const { __syncwarp(); }
+  template <class T>
+  MF_FN void put(T* p, T v) const {
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) *p = v;
+    __syncwarp();
+  }
+  MF_FN int shfl_xor(int v, int m) const { return __shfl_xor_sync(0xffffffffu, v, m); }
+  MF_FN unsigned shfl_xor(unsigned v, int m) const { return __shfl_xor_sync(0xffffffffu, v, m); }
+  MF_FN double shfl_xor(double v, int m) const { return __shfl_xor_sync(0xffffffffu, v, m); }
+  MF_FN uint64_t shfl_xor(uint64_t v, int m) const {
+    return (uint64_t)__shfl_xor_sync(0xffffffffu, (unsigned long long)v, m);
+  }
+  MF_FN long long shfl_xor(long long v, int m) const { return __shfl_xor_sync(0xffffffffu, v, m); }
+  MF_FN int shfl(int v, int src) const { return __shfl_sync(0xffffffffu, v, src); }
+  MF_FN double shfl(double v, int src) const { return __shfl_sync(0xffffffffu, v, src); }
+  MF_FN uint64_t shfl(uint64_t v, int src) const {
+    return (uint64_t)__shfl_sync(0xffffffffu, (unsigned long long)v, src);
+  }
+  MF_FN int shfl_up(int v, int d) const { return __shfl_up_sync(0xffffffffu, v, d); }
+  MF_FN unsigned ballot(bool p) const { return __ballot_sync(0xffffffffu, p); }
+  MF_FN bool any(bool p) const { return __any_sync(0xffffffffu, p); }
+  MF_FN int sum(int v) const { return __reduce_add_sync(0xffffffffu, (unsigned)v); }
+  MF_FN int atomic_add(int* p, int v) const { return atomicAdd(p, v); }
+  MF_FN unsigned atomic_or(unsigned* p, unsigned v) const { return atomicOr(p, v); }
+  // exclusive prefix sum of v over lanes; *total receives the warp sum
+  MF_FN int excl_scan(int v, int* total) const {
+    int x = v;
+    const int l = threadIdx.x & 31;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      int y = __shfl_up_sync(0xffffffffu, x, d);
+      if (l >= d) x += y;
+    }
+    *total = __shfl_sync(0xffffffffu, x, 31);
+    return x - v;
+  }
+};
+#endif
+
+struct SerialLanes {
+  static constexpr int N = 1;
+  inline int lane() const { return 0; }
+  inline bool leader() const { return true; }
+  inline void sync() const {}
+  template <class T>
+  inline void put(T* p, T v) const { *p = v; }
+  template <class T>
+  inline T shfl_xor(T v, int) const { return v; }
+  template <class T>
+  inline T shfl(T v, int) const { return v; }
+  inline int shfl_up(int v, int) const { return v; }
+  inline unsigned ballot(bool p) const { return p ? 1u : 0u; }
+  inline bool any(bool p) const { return p; }
+  inline int sum(int v) const { return v; }
+  inline int atomic_add(int* p, int v) const {
+    int o = *p;
+    *p = o + v;
+    return o;
+  }
+  inline unsigned atomic_or(unsigned* p, unsigned v) const {
+    unsigned o = *p;
+    *p = o | v;
+    return o;
+  }
+  inline int excl_scan(int v, int* total) const {
+    *total = v;
+    return 0;
+  }
+};
+
+}  // namespace mfb
