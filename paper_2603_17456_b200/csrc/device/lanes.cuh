@@ -38,14 +38,14 @@ struct WarpLanes {
   MF_FN int shfl_xor(int v, int m) const { return __shfl_xor_sync(0xffffffffu, v, m); }
   MF_FN unsigned shfl_xor(unsigned v, int m) const { return __shfl_xor_sync(0xffffffffu, v, m); }
   MF_FN double shfl_xor(double v, int m) const { return __shfl_xor_sync(0xffffffffu, v, m); }
-  MF_FN uint64_t shfl_xor(uint64_t v, int m) const {
-    return (uint64_t)__shfl_xor_sync(0xffffffffu, (unsigned long long)v, m);
+  MF_FN unsigned long long shfl_xor(unsigned long long v, int m) const {
+    return __shfl_xor_sync(0xffffffffu, v, m);
   }
   MF_FN long long shfl_xor(long long v, int m) const { return __shfl_xor_sync(0xffffffffu, v, m); }
   MF_FN int shfl(int v, int src) const { return __shfl_sync(0xffffffffu, v, src); }
   MF_FN double shfl(double v, int src) const { return __shfl_sync(0xffffffffu, v, src); }
-  MF_FN uint64_t shfl(uint64_t v, int src) const {
-    return (uint64_t)__shfl_sync(0xffffffffu, (unsigned long long)v, src);
+  MF_FN unsigned long long shfl(unsigned long long v, int src) const {
+    return __shfl_sync(0xffffffffu, v, src);
   }
   MF_FN int shfl_up(int v, int d) const { return __shfl_up_sync(0xffffffffu, v, d); }
   MF_FN unsigned ballot(bool p) const { return __ballot_sync(0xffffffffu, p); }
