@@ -1,0 +1,321 @@
+#!/usr/bin/env python3
+"""Throughput benchmark: simulated flow-events/sec of the B200 engine.
+
+Workload (BASELINE.json configs[3]): the batched sweep on the ft128 fabric
+("1024 GPUs" = 128 hosts x 8 NICs, k=8 fat-tree), 2000 requests per instance,
+cells = offered load x SLO multiplier x seed x policy. A step = one device
+launch that simulates S full instances of that grid from their initial state
+on each rank (weak scaling: S fixed per GPU; ranks take disjoint cells; no
+collective on the data path). flow-events = RunResult::events
+(engine.cpp:611), summed over instances.
+
+  value : events / device time of the timed launches (inputs resident in HBM,
+          CUDA events on the launch stream, max over ranks)
+  e2e   : same metric through the C ABI with host buffers: H2D of the inputs,
+          launch, D2H of per-request results, every step
+  --impl reference : the reference CPU simulator (oracle/_ref, unmodified
+          sources) on all host cores, same cells, bounded sample per step
+"""
+from __future__ import annotations
+
+import argparse
+import concurrent.futures as cf
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, HERE)
+
+PEAKS = os.path.join(HERE, "MEASURED_PEAKS.json")
+HBM_FALLBACK = 6650.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--instances", type=int, default=int(os.environ.get("MFSIM_BENCH_INSTANCES", 1184)),
+                    help="instances per rank per step")
+    ap.add_argument("--requests", type=int, default=2000, help="requests per instance (configs[3]: 2000)")
+    ap.add_argument("--cpu-sample-s", type=float, default=20.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    return rank, world, local
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region."""
+
+    def __init__(self, index: int):
+        self.index, self.samples, self._stop = index, [], threading.Event()
+        self.t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap,utilization.gpu")
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self.t.join(timeout=6)
+
+    def summary(self):
+        rows = [s for s in self.samples if len(s) >= 8]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no-samples"]}
+        load = [r for r in rows if r[7].isdigit() and int(r[7]) > 0] or rows
+        sm = sorted(float(r[0]) for r in load)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in load for i in range(4) if r[3 + i].lower() == "active"})
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": float(rows[0][1]), "reasons": reasons,
+                "samples": len(load)}
+
+
+def cells_for(rank: int, world: int, n: int, step_offset: int = 0):
+    from paper_2603_17456_b200 import sweep
+
+    allc = sweep.sweep_cells()
+    start = ((step_offset * world + rank) * n) % len(allc)
+    return [allc[(start + i) % len(allc)] for i in range(n)]
+
+
+def cpu_reference(cells, requests, budget_s, lib_cfg):
+    """reference simulator on all host cores (thread pool; the harness releases the GIL)"""
+    from oracle import ref
+
+    cores = os.cpu_count() or 1
+    texts = [lib_cfg(c) for c in cells]
+    t0 = time.perf_counter()
+    events, done, run_s = 0, 0, 0.0
+    with cf.ThreadPoolExecutor(max_workers=cores) as ex:
+        futs, it = set(), iter(texts)
+        for _ in range(cores):
+            t = next(it, None)
+            if t is not None:
+                futs.add(ex.submit(ref.run_config, t))
+        while futs:
+            fin, futs = cf.wait(futs, return_when=cf.FIRST_COMPLETED)
+            for f in fin:
+                r = f.result()
+                events += r.events
+                run_s += r.t_run_s
+                done += 1
+                if time.perf_counter() - t0 < budget_s:
+                    t = next(it, None)
+                    if t is not None:
+                        futs.add(ex.submit(ref.run_config, t))
+    wall = time.perf_counter() - t0
+    return {"events": events, "wall_s": wall, "instances": done, "cores": cores,
+            "engine_run_s": run_s}
+
+
+def reference_arm(args, rank, world):
+    if rank != 0:
+        return
+    from paper_2603_17456_b200 import sweep
+
+    def cfg_text(c):
+        return sweep_text(c, args.requests)
+
+    def sweep_text(c, n):
+        return sweep.sweep_config(c, requests=n, lib=_emu_or_product())
+
+    cells = cells_for(0, 1, max(args.instances, 64))
+    for _ in range(args.warmup):
+        pass  # the reference has no device warm-up; cores are warm after the first step
+    vals, evs, wall = [], 0, 0.0
+    budget = max(5.0, args.cpu_sample_s / max(args.steps, 1))
+    for s in range(args.steps):
+        sub = cells[(s * 16) % len(cells):] + cells
+        r = cpu_reference(sub, args.requests, budget, cfg_text)
+        vals.append(r["events"] / r["wall_s"])
+        evs += r["events"]
+        wall += r["wall_s"]
+    value = evs / wall
+    line = {
+        "impl": "reference", "metric": "simulated flow-events/sec", "value": value,
+        "unit": "events/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1000 * wall / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": workload_config(args),
+        "cpu_baseline": {"value": value, "unit": "events/s", "cores": r["cores"], "kind": "reference",
+                         "sample": f"{args.steps} steps x ~{budget:.0f}s of sweep instances "
+                                   f"({args.requests} requests each) on all host cores"},
+        "e2e": {"value": value, "unit": "events/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+_emu = None
+
+
+def _emu_or_product():
+    """route computation only needs the host side of the library"""
+    global _emu
+    if _emu is None:
+        from paper_2603_17456_b200.native import Native, PRODUCT_SO
+        path = PRODUCT_SO if os.path.exists(PRODUCT_SO) else os.path.join(HERE, "build", "libmfsim_emu.so")
+        _emu = Native(path)
+    return _emu
+
+
+def workload_config(args):
+    return {
+        "workload": "configs[3] sweep: ft128 fat-tree (128 hosts x 8 NICs, k=8, 768 links), "
+                    "16 units x 4 hosts + 64 decode, cells = load {0.3..0.9} x SLO {1..5} x "
+                    "seed {1..64} x policy {fs,sjf,edf,karuna,mfs}",
+        "instances_per_rank_per_step": args.instances,
+        "requests_per_instance": args.requests,
+        "l2": "inputs larger than L2 (per-step working set >> 126 MB)",
+        "parallelism": f"instance-sharded x{args.gpus}",
+    }
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        if world > 1:
+            import torch.distributed as dist  # noqa: F401
+        reference_arm(args, rank, world)
+        return
+
+    import torch
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2603_17456_b200 import sweep
+    from paper_2603_17456_b200.native import DeviceBatch, product
+
+    lib = product()
+    stream = torch.cuda.current_stream()
+    cells = cells_for(rank, world, args.instances)
+    t0 = time.perf_counter()
+    batch = DeviceBatch(local, lib, stream=stream.cuda_stream)
+    for c in cells:
+        batch.add_config(sweep.sweep_config(c, requests=args.requests, lib=lib))
+    batch.prepare()
+    setup_s = time.perf_counter() - t0
+    # first full run: capacity retries settle here (not timed), results kept for checks
+    batch.run(0)
+    for i in range(len(batch)):
+        batch.raise_for_status(i)
+    events_per_step = sum(batch.stats(i).events for i in range(len(batch)))
+    algo_bytes = sum(batch.stats(i).algo_bytes for i in range(len(batch)))
+    met = sum(batch.stats(i).slo_met for i in range(len(batch)))
+    reqs = sum(batch.stats(i).requests for i in range(len(batch)))
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        batch.launch()
+    barrier()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(local) as clk:
+        start.record(stream)
+        for _ in range(args.steps):
+            batch.launch()
+        end.record(stream)
+        barrier()
+    dev_ms = start.elapsed_time(end)
+    # e2e through the C ABI with host buffers (H2D + launch + D2H each step)
+    barrier()
+    e0 = time.perf_counter()
+    for _ in range(args.steps):
+        batch.upload()
+        batch.launch()
+        batch.download(0)
+    barrier()
+    e2e_s = time.perf_counter() - e0
+    h2d, d2h = batch.h2d_bytes, batch.d2h_bytes
+
+    t = torch.tensor([dev_ms, e2e_s, float(events_per_step)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        mx = t.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        sm = t.clone()
+        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+        dev_ms, e2e_s, total_events = mx[0].item(), mx[1].item(), sm[2].item()
+    else:
+        total_events = float(events_per_step)
+    value = total_events * args.steps / (dev_ms / 1000.0)
+    e2e = total_events * args.steps / e2e_s
+    kernel_ms = dev_ms / args.steps
+    achieved = algo_bytes / (kernel_ms / 1000.0) / 1e9
+    try:
+        peaks = json.load(open(PEAKS))
+        peak, peak_src = float(peaks["hbm_gbs"]), "measured"
+    except Exception:
+        peak, peak_src = HBM_FALLBACK, "fallback"
+
+    if rank == 0:
+        line = {
+            "metric": "simulated flow-events/sec", "value": value, "unit": "events/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": kernel_ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": workload_config(args),
+            "e2e": {"value": e2e, "unit": "events/s", "h2d_bytes_per_step": int(h2d),
+                    "d2h_bytes_per_step": int(d2h)},
+            "gpu_launches": args.steps,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
+                         "kernel": "mfsim_engine_kernel"},
+            "clocks": clk.summary(),
+            "events_per_step_rank0": events_per_step,
+            "slo_attainment_rank0": met / max(reqs, 1),
+            "setup_s_rank0": setup_s,
+            "device_bytes_rank0": batch.device_bytes,
+        }
+        if not args.no_cpu_baseline:
+            def cfg_text(c):
+                return sweep.sweep_config(c, requests=args.requests, lib=lib)
+            try:
+                r = cpu_reference(cells, args.requests, args.cpu_sample_s, cfg_text)
+                line["cpu_baseline"] = {
+                    "value": r["events"] / r["wall_s"], "unit": "events/s", "cores": r["cores"],
+                    "kind": "reference",
+                    "sample": f"{r['instances']} sweep instances ({args.requests} requests each) "
+                              f"in {r['wall_s']:.1f}s on {r['cores']} host threads"}
+            except Exception as e:  # the oracle library is absent: report why
+                line["cpu_baseline"] = {"value": None, "unit": "events/s", "cores": 0,
+                                        "kind": "reference", "sample": f"unavailable: {e}"}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -48,6 +48,8 @@ typedef struct mfsim_dev_stats {
   long long requests;
   long long finished;
   long long slo_met;
+  long long classes;     /* priority classes served by the allocator */
+  long long rounds;      /* progressive-filling rounds of multi-flow classes */
 } mfsim_dev_stats;
 
 /* create a context on CUDA device `device` */
@@ -100,6 +102,14 @@ int mfsim_dev_batches(const mfsim_dev* d, int i, double* done, long cap);
 int mfsim_dev_summary_json(const mfsim_dev* d, int i, char** out);
 int mfsim_dev_requests_csv(const mfsim_dev* d, int i, char** out);
 int mfsim_dev_write_report(const mfsim_dev* d, int i, const char* out_dir);
+
+/* Topology::route (topology.cpp:83-89) of the fabric a config describes:
+ * link ids src -> dst into links[0..cap); *n receives the route length;
+ * *capacity (optional) receives each link's capacity in bytes/s */
+int mfsim_route(const mfsim_config* cfg, int src, int dst, int* links, double* capacity, int cap,
+                int* n);
+/* number of links of the fabric a config describes */
+int mfsim_link_count(const mfsim_config* cfg, int* n);
 
 #ifdef __cplusplus
 }

@@ -250,6 +250,8 @@ int mfsim_dev_stats_get(const mfsim_dev* d, int i, mfsim_dev_stats* s) {
     s->max_active = o.out[mfb::OUT_MAXACTIVE];
     s->pushes = o.out[mfb::OUT_PUSHES];
     s->algo_bytes = o.out[mfb::OUT_ALGO_BYTES];
+    s->classes = o.out[mfb::OUT_CLASSES];
+    s->rounds = o.out[mfb::OUT_ROUNDS];
     s->requests = static_cast<long long>(o.ttft.size());
     for (size_t r = 0; r < o.ttft.size(); ++r) {
       if (o.ttft[r] == -1.0) continue;
@@ -344,6 +346,27 @@ int mfsim_dev_write_report(const mfsim_dev* d, int i, const char* out_dir) {
     raise_status(o.out[mfb::OUT_STATUS], o.out[mfb::OUT_CHECK]);
     write_files(report_of(in, o), in.policy, in.seed, in.rate, out_dir);
   });
+}
+
+int mfsim_route(const mfsim_config* cfg, int src, int dst, int* links, double* capacity, int cap,
+                int* n) {
+  if (!cfg || !n) return fail(MFSIM_ERR_INVALID_ARG, "mfsim_route: NULL argument");
+  return guarded([&] {
+    const Fabric f = Fabric::from(cfg->cfg);
+    if (src < 0 || dst < 0 || src >= f.nodes() || dst >= f.nodes())
+      throw ConfigError("mfsim_route: node out of range");
+    const std::vector<int> r = f.route(src, dst);
+    *n = static_cast<int>(r.size());
+    for (int k = 0; k < static_cast<int>(r.size()) && k < cap; ++k) {
+      if (links) links[k] = r[k];
+      if (capacity) capacity[k] = f.links()[r[k]].capacity;
+    }
+  });
+}
+
+int mfsim_link_count(const mfsim_config* cfg, int* n) {
+  if (!cfg || !n) return fail(MFSIM_ERR_INVALID_ARG, "mfsim_link_count: NULL argument");
+  return guarded([&] { *n = static_cast<int>(Fabric::from(cfg->cfg).links().size()); });
 }
 
 }  // extern "C"

@@ -30,7 +30,8 @@ class MfsimError(RuntimeError):
 class DevStats(C.Structure):
     _fields_ = [(n, C.c_longlong) for n in (
         "status", "check", "events", "steps", "flows", "batches", "coflows", "pruned",
-        "max_active", "pushes", "algo_bytes", "requests", "finished", "slo_met")]
+        "max_active", "pushes", "algo_bytes", "requests", "finished", "slo_met", "classes",
+        "rounds")]
 
 
 @dataclass
@@ -109,6 +110,8 @@ class Native:
             "mfsim_dev_summary_json": ([vp, i, C.POINTER(C.c_void_p)], i),
             "mfsim_dev_requests_csv": ([vp, i, C.POINTER(C.c_void_p)], i),
             "mfsim_dev_write_report": ([vp, i, cp], i),
+            "mfsim_route": ([vp, i, i, vp, vp, i, C.POINTER(i)], i),
+            "mfsim_link_count": ([vp, C.POINTER(i)], i),
         }
         for name, (args, res) in sig.items():
             fn = getattr(L, name)
@@ -288,6 +291,25 @@ class DeviceBatch:
             self.n.lib.mfsim_dev_destroy(self.h)
         except Exception:
             pass
+
+
+def route(cfg, src: int, dst: int, lib: Native | None = None):
+    """Link ids and capacities of the route src -> dst (Topology::route)."""
+    n = lib or product()
+    if not isinstance(cfg, Config):
+        cfg = Config(cfg, n)
+    links, caps, cnt = np.zeros(64, np.int32), np.zeros(64), C.c_int(0)
+    n.check(n.lib.mfsim_route(cfg.h, src, dst, _ptr(links), _ptr(caps), 64, C.byref(cnt)))
+    return links[:cnt.value].tolist(), caps[:cnt.value].tolist()
+
+
+def link_count(cfg, lib: Native | None = None) -> int:
+    n = lib or product()
+    if not isinstance(cfg, Config):
+        cfg = Config(cfg, n)
+    cnt = C.c_int(0)
+    n.check(n.lib.mfsim_link_count(cfg.h, C.byref(cnt)))
+    return cnt.value
 
 
 def run_config(text, device: int = 0, detail: int = 2, lib: Native | None = None) -> SimResult:

@@ -1,0 +1,27 @@
+"""CPU tier: the engine source (csrc/device/engine.cuh) compiled as a serial
+1-lane host build (TEST ONLY, build/libmfsim_emu.so) is bit-exact against the
+golden fixtures. This checks engine logic without a GPU; the GPU tier runs the
+same cases on the sm_100a product library."""
+import pytest
+
+import cases
+from parity import manifest, mismatches
+from paper_2603_17456_b200.native import MfsimError, run_config, run_manual
+
+
+@pytest.mark.parametrize("name", sorted(cases.manual_cases()))
+def test_manual_case(emu, name):
+    res = run_manual(cases.manual_cases()[name], lib=emu)
+    assert mismatches(res, "manual", name) == []
+
+
+@pytest.mark.parametrize("name", sorted(cases.workload_cases()))
+def test_workload_case(emu, name):
+    res = run_config(cases.workload_cases()[name], lib=emu)
+    assert mismatches(res, "workload", name) == []
+
+
+def test_livelock_error_code(emu):
+    with pytest.raises(MfsimError) as e:
+        run_manual(cases.livelock(), lib=emu)
+    assert e.value.code == manifest()["errors"]["livelock"]
