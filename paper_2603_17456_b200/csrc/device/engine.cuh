@@ -81,6 +81,13 @@ MF_FN unsigned long long dord(double x) {
   unsigned long long u = dbits(x);
   return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
 }
+#if defined(__CUDACC__)
+MF_FN int ctz32(unsigned m) { return __ffs(m) - 1; }
+MF_FN int popc32(unsigned m) { return __popc(m); }
+#else
+MF_FN int ctz32(unsigned m) { return __builtin_ctz(m); }
+MF_FN int popc32(unsigned m) { return __builtin_popcount(m); }
+#endif
 MF_FN int klass_of(int kind) { return kind <= EV_DEPART ? 0 : (kind == EV_TICK ? 2 : 1); }
 MF_FN int pow2ceil(int n) {
   int p = 1;
@@ -101,6 +108,7 @@ struct Sc {
   unsigned epoch;
   int n_live;
   int h_n, h_ready;
+  int n_srt, n_add;
   int dirty;
   int err, chk;
   long long pruned;
@@ -124,10 +132,10 @@ MF_FN bool ev_less(const Ev& x, const Ev& y) {
 template <class G>
 struct Engine {
   G g;
-  const Inst& I;
+  Inst& I;  // per-warp copy (shared memory on the device), arrays possibly re-pointed
   Sc s;
 
-  MF_FN explicit Engine(const Inst& inst) : I(inst) {}
+  MF_FN explicit Engine(Inst& inst) : I(inst) {}
 
   // ----------------------------------------------------------------- util
   template <class T>
@@ -138,12 +146,18 @@ struct Engine {
       s.chk = chk;
     }
   }
-  MF_FN int rbeg(int fid) const { return I.route_off[I.f_route[fid]]; }
+  MF_FN int rbeg(int fid) const {
+    const int r = I.f_route[fid];
+    return r >= 0 ? I.route_off[r] : 0;
+  }
   MF_FN int rlen(int fid) const {
-    int r = I.f_route[fid];
-    return I.route_off[r + 1] - I.route_off[r];
+    const int r = I.f_route[fid];
+    return r >= 0 ? I.route_off[r + 1] - I.route_off[r] : 0;
   }
   MF_FN bool done(int fid) const { return I.f_state[fid] == FL_DONE; }
+  // cached route of the active flow at position p
+  MF_FN int arl(int p, int k) const { return I.a_rl[p * I.rmax + k]; }
+  MF_FN int arn(int p) const { return I.a_rn[p]; }
   MF_FN double remaining(int fid) const {
     int p = I.f_apos[fid];
     if (p >= 0) return I.a_rem[p];
@@ -238,9 +252,12 @@ struct Engine {
       I.a_rate[pos] = I.a_rate[last];
       I.a_evt[pos] = I.a_evt[last];
       I.a_evseq[pos] = I.a_evseq[last];
+      I.a_rn[pos] = I.a_rn[last];
       I.f_apos[lf] = pos;
       I.f_apos[fid] = -1;
     }
+    const int rm = I.rmax;
+    for (int k = g.lane(); k < rm; k += G::N) I.a_rl[pos * rm + k] = I.a_rl[last * rm + k];
     g.sync();
     --s.n_active;
   }
@@ -273,27 +290,56 @@ struct Engine {
   }
 
   // --------------------------------------------------------- pipeline info
-  MF_FN int l_curr(int b) const {  // engine.cpp:712-720
+  // per-layer scans run one layer per lane (votes), layers in order
+  MF_FN int l_curr(int b) {  // engine.cpp:712-720
     const int L = I.b_layers[b];
     const int base = I.b_lbase[b];
-    for (int l = 1; l <= L; ++l) {
-      int idx = base + l - 1;
-      if (!I.pl_done[idx]) return l;
-      int c = I.pl_coll[idx];
-      if (c >= 0 && I.c_open[c] > 0) return l;
+    for (int l0 = 0; l0 < L; l0 += G::N) {
+      const int l = l0 + g.lane();
+      bool hit = false;
+      if (l < L) {
+        const int c = I.pl_coll[base + l];
+        hit = !I.pl_done[base + l] || (c >= 0 && I.c_open[c] > 0);
+      }
+      const unsigned m = g.ballot(hit);
+      if (m) return l0 + ctz32(m) + 1;
     }
     return L > 1 ? L : 1;
   }
-  MF_FN double remaining_compute(int b) const {  // engine.cpp:722-728
+  MF_FN double remaining_compute(int b) {  // engine.cpp:722-728, summed in layer order
     const int L = I.b_layers[b];
     const int base = I.b_lbase[b];
     double total = 0.0;
-    for (int i = 0; i < L; ++i)
-      if (!I.pl_done[base + i]) total = dadd(total, I.pl_cost[base + i]);
+    for (int l0 = 0; l0 < L; l0 += G::N) {
+      const int l = l0 + g.lane();
+      double v = 0.0;
+      bool use = false;
+      if (l < L) {
+        use = !I.pl_done[base + l];
+        v = I.pl_cost[base + l];
+      }
+      const unsigned m = g.ballot(use);
+      const int cnt = (L - l0) < G::N ? (L - l0) : G::N;
+      for (int k = 0; k < cnt; ++k) {
+        const double x = g.shfl(v, k);
+        if (m & (1u << k)) total = dadd(total, x);
+      }
+    }
     return total;
   }
   MF_FN bool batch_drained(int b) const {  // engine.cpp:730-734
     return I.b_done[b] != kNoTime && I.b_open[b] == 0;
+  }
+  // all layers computed and every collective closed (engine.cpp:387-390)
+  MF_FN bool pipeline_complete(int b) {
+    const int L = I.b_layers[b];
+    const int base = I.b_lbase[b];
+    bool bad = false;
+    for (int l = g.lane(); l < L; l += G::N) {
+      const int c = I.pl_coll[base + l];
+      if (!I.pl_done[base + l] || (c >= 0 && I.c_open[c] > 0)) bad = true;
+    }
+    return !g.any(bad);
   }
 
   // ========================================================= K2: RMLQ
@@ -315,16 +361,15 @@ struct Engine {
     for (int base = 0; base < s.n_active; base += G::N) {
       int p = base + g.lane();
       int c = 0;
-      if (p < s.n_active && I.a_rate[p] > 0.0) c = rlen(I.a_fid[p]);
+      if (p < s.n_active && I.a_rate[p] > 0.0) c = arn(p);
       int tot;
       int off = g.excl_scan(c, &tot);
       if (c > 0) {
         int fid = I.a_fid[p];
-        int rb = rbeg(fid);
         unsigned long long key = ((unsigned long long)I.f_band[fid] << 16) | I.f_level[fid];
         double r = I.a_rate[p];
         for (int k = 0; k < c; ++k) {
-          int l = I.route_links[rb + k];
+          int l = arl(p, k);
           I.x_hi[total + off + k] = ((unsigned long long)l << 32) | key;
           I.x_lo[total + off + k] = dbits(r);
           I.x_val[total + off + k] = r;
@@ -453,9 +498,9 @@ struct Engine {
       if (p < s.n_active && I.a_rate[p] > 0.0) {
         int fid = I.a_fid[p];
         if (outranks(I.f_band[fid], I.f_level[fid], band, level)) {
-          int rb = rbeg(fid), rn = rlen(fid);
+          const int rn = arn(p);
           for (int k = 0; k < rn; ++k)
-            if (I.route_links[rb + k] == l) {
+            if (arl(p, k) == l) {
               c = 1;
               break;
             }
@@ -727,50 +772,56 @@ struct Engine {
   // ================================================= K3: decide (policies)
   // Fills s_ord (class order of active positions), s_cls (class starts, with
   // sentinel) and s_cap; returns the number of classes and *has_caps.
+  //
+  // Sorted policies keep the previous step's order (srt, flow ids) plus the
+  // flows released since (srt_add): if the surviving old order is still sorted
+  // under the current keys, the new flows are merged in (O(A) per step);
+  // otherwise the subset is fully re-sorted. Keys end in the flow id, so the
+  // order is total and equals the reference's std::sort result either way.
   MF_NOINLINE int decide(bool* has_caps) {
     *has_caps = false;
     const int A = s.n_active;
-    if (A == 0) return 0;
+    if (A == 0) {
+      s.n_srt = 0;
+      s.n_add = 0;
+      return 0;
+    }
     const int pol = I.p.policy;
     int ncls = 0;
     if (pol == POL_FS) {  // baselines.cpp:46-51
       for (int p = g.lane(); p < A; p += G::N) I.s_ord[p] = p;
+      if (g.leader()) I.s_cls[0] = 0;
       g.sync();
-      I.s_cls[0] = 0;  // benign identical writes
       ncls = 1;
     } else if (pol == POL_SJF) {  // baselines.cpp:23-57
       for (int p = g.lane(); p < A; p += G::N) {
-        int fid = I.a_fid[p];
-        I.s_ord[p] = p;
         I.s_k0[p] = dord(I.a_rem[p]);
-        I.s_k1[p] = dord(I.f_rel[fid]);
+        I.s_k1[p] = dord(I.f_rel[I.a_fid[p]]);
         I.s_k2[p] = 0;
         I.s_k3[p] = 0;
       }
       g.sync();
-      sort_ord(I.s_ord, A);
-      ncls = group_classes(0, A, 0);
+      const int n = sorted_subset(I.s_ord, [&](int) { return true; });
+      ncls = group_classes(0, n, 0);
     } else if (pol == POL_EDF) {  // baselines.cpp:59-90
-      int ne = compact(I.s_ord, [&](int p) { return has_dl(I.a_fid[p]); });
-      for (int i = g.lane(); i < ne; i += G::N) {
-        int p = I.s_ord[i];
-        int fid = I.a_fid[p];
+      for (int p = g.lane(); p < A; p += G::N) {
+        const int fid = I.a_fid[p];
         I.s_k0[p] = dord(I.f_dl[fid]);
         I.s_k1[p] = dord(I.f_rel[fid]);
         I.s_k2[p] = 0;
         I.s_k3[p] = 0;
       }
       g.sync();
-      sort_ord(I.s_ord, ne);
+      const int ne = sorted_subset(I.s_ord, [&](int p) { return has_dl(I.a_fid[p]); });
       ncls = group_classes(0, ne, 0);
-      int ni = compact(I.s_ord + ne, [&](int p) { return !has_dl(I.a_fid[p]); });
+      const int ni = compact(I.s_ord + ne, [&](int p) { return !has_dl(I.a_fid[p]); });
       if (ni > 0) {
         if (g.leader()) I.s_cls[ncls] = ne;
         g.sync();
         ++ncls;
       }
     } else if (pol == POL_KARUNA) {  // baselines.cpp:92-135
-      int nd = compact(I.s_ord, [&](int p) { return has_dl(I.a_fid[p]); });
+      const int nd = compact(I.s_ord, [&](int p) { return has_dl(I.a_fid[p]); });
       if (nd > 0) {
         karuna_caps(nd);
         if (s.err) return 0;
@@ -779,24 +830,22 @@ struct Engine {
         g.sync();
         ncls = 1;
       }
-      int nr = compact(I.s_ord + nd, [&](int p) { return !has_dl(I.a_fid[p]); });
-      for (int i = g.lane(); i < nr; i += G::N) {
-        int p = I.s_ord[nd + i];
+      for (int p = g.lane(); p < A; p += G::N) {
         I.s_k0[p] = dord(I.a_rem[p]);
         I.s_k1[p] = dord(I.f_rel[I.a_fid[p]]);
         I.s_k2[p] = 0;
         I.s_k3[p] = 0;
       }
       g.sync();
-      sort_ord(I.s_ord + nd, nr);
+      const int nr = sorted_subset(I.s_ord + nd, [&](int p) { return !has_dl(I.a_fid[p]); });
       ncls = group_classes(nd, nr, ncls);
     } else {  // MFS arbitrate (rmlq.cpp:201-260)
       for (int p = g.lane(); p < A; p += G::N) {
-        int fid = I.a_fid[p];
-        int band = I.f_band[fid];
+        const int fid = I.a_fid[p];
+        const int band = I.f_band[fid];
         double dl = I.f_dl[fid];
         if (isnan_(dl)) {
-          int r = I.f_req[fid];
+          const int r = I.f_req[fid];
           dl = r >= 0 ? I.r_deadline[r] : MF_INF;
         }
         double k1 = 0.0, k2 = 0.0, k3 = 0.0;
@@ -810,20 +859,111 @@ struct Engine {
         } else {
           k1 = dl;
         }
-        I.s_ord[p] = p;
         I.s_k0[p] = (unsigned long long)band;
         I.s_k1[p] = dord(k1);
         I.s_k2[p] = dord(k2);
         I.s_k3[p] = dord(k3);
       }
       g.sync();
-      sort_ord(I.s_ord, A);
-      ncls = group_classes(0, A, 0);
+      const int n = sorted_subset(I.s_ord, [&](int) { return true; });
+      ncls = group_classes(0, n, 0);
     }
     if (g.leader()) I.s_cls[ncls] = A;
     g.sync();
     s.algo_bytes += 40LL * A;
     return ncls;
+  }
+
+  // Sorted list of the active positions p with in_subset(p), written to ord.
+  template <class P>
+  MF_FN int sorted_subset(int* ord, P in_subset) {
+    if (s.n_add < 0) {  // add list overflowed: sort every member from scratch
+      const int n = compact(ord, in_subset);
+      sort_ord(ord, n);
+      for (int i = g.lane(); i < n; i += G::N) I.srt[i] = I.a_fid[ord[i]];
+      g.sync();
+      s.n_srt = n;
+      s.n_add = 0;
+      return n;
+    }
+    // survivors of the previous order, in that order
+    int n1 = 0;
+    for (int base = 0; base < s.n_srt; base += G::N) {
+      const int i = base + g.lane();
+      int p = -1;
+      if (i < s.n_srt) p = I.f_apos[I.srt[i]];
+      const bool keep = p >= 0 && in_subset(p);
+      const unsigned m = g.ballot(keep);
+      if (keep) ord[n1 + popc32(m & ((1u << g.lane()) - 1u))] = p;
+      n1 += popc32(m);
+    }
+    // flows released since, still active and in the subset
+    int n2 = 0;
+    int* add = ord + n1;  // staged right after the survivors
+    for (int base = 0; base < s.n_add; base += G::N) {
+      const int i = base + g.lane();
+      int p = -1;
+      if (i < s.n_add) p = I.f_apos[I.srt_add[i]];
+      const bool keep = p >= 0 && in_subset(p);
+      const unsigned m = g.ballot(keep);
+      if (keep) add[n2 + popc32(m & ((1u << g.lane()) - 1u))] = p;
+      n2 += popc32(m);
+    }
+    g.sync();
+    const int n = n1 + n2;
+    // still sorted? (keys may have changed since the last step)
+    bool broken = false;
+    for (int i = 1 + g.lane(); i < n1; i += G::N)
+      if (pos_less(ord[i], ord[i - 1])) broken = true;
+    if (g.any(broken) || n2 > 64) {
+      sort_ord(ord, n);
+    } else if (n2 > 0) {
+      // insertion sort of the few new flows, then a merge by ranks
+      if (g.leader()) {
+        for (int a = 1; a < n2; ++a) {
+          const int v = add[a];
+          int m = a;
+          while (m > 0 && pos_less(v, add[m - 1])) {
+            add[m] = add[m - 1];
+            --m;
+          }
+          add[m] = v;
+        }
+      }
+      g.sync();
+      int* tmp = I.s_ul;  // scratch (free outside allocate)
+      for (int i = g.lane(); i < n; i += G::N) {
+        const int v = ord[i];
+        int lo, hi, dst;
+        if (i < n1) {  // rank among the new flows
+          lo = 0;
+          hi = n2;
+          while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (pos_less(add[mid], v)) lo = mid + 1; else hi = mid;
+          }
+          dst = i + lo;
+        } else {  // rank among the survivors
+          lo = 0;
+          hi = n1;
+          while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (pos_less(ord[mid], v)) lo = mid + 1; else hi = mid;
+          }
+          dst = (i - n1) + lo;
+        }
+        tmp[dst] = v;
+      }
+      g.sync();
+      for (int i = g.lane(); i < n; i += G::N) ord[i] = tmp[i];
+      g.sync();
+    }
+    // remember this order (flow ids) for the next step
+    for (int i = g.lane(); i < n; i += G::N) I.srt[i] = I.a_fid[ord[i]];
+    g.sync();
+    s.n_srt = n;
+    s.n_add = 0;
+    return n;
   }
 
   // Karuna caps for the deadline class s_ord[0, nd): per-link demand summed in
@@ -845,15 +985,14 @@ struct Engine {
         double slack = dsub(I.f_dl[fid], s.now);
         if (slack > 0.0) {
           want = ddiv(I.a_rem[p], slack);
-          c = rlen(fid);
+          c = arn(p);
         }
       }
       int tot;
       int off = g.excl_scan(c, &tot);
       if (c > 0) {
-        int rb = rbeg(fid);
         for (int k = 0; k < c; ++k) {
-          int l = I.route_links[rb + k];
+          int l = arl(p, k);
           I.x_hi[total + off + k] = ((unsigned long long)l << 32) | (unsigned)p;
           I.x_lo[total + off + k] = 0;
           I.x_val[total + off + k] = want;
@@ -902,9 +1041,9 @@ struct Engine {
       if (!(slack > 0.0)) continue;
       double want = I.s_rate[p];
       double scale = 1.0;
-      int rb = rbeg(fid), rn = rlen(fid);
+      const int rn = arn(p);
       for (int k = 0; k < rn; ++k) {
-        int l = I.route_links[rb + k];
+        int l = arl(p, k);
         double c = I.cap[l];
         double dmd = I.l_x[l];
         if (dmd > c) scale = smin(scale, ddiv(c, dmd));
@@ -915,24 +1054,15 @@ struct Engine {
   }
 
   // ============================================ K3: strict-priority filling
-  MF_FN double residual(int l) const {
-    return I.l_stamp[l] == s.epoch ? I.l_res[l] : I.cap[l];
-  }
-  MF_FN void set_residual(int l, double v) {
-    I.l_res[l] = v;
-    I.l_stamp[l] = s.epoch;
-  }
-
-  // allocator.cpp:28-126 over the classes in s_ord/s_cls; rates -> s_rate
+  // allocator.cpp:28-126. Invariants outside this function: l_res == capacity
+  // and l_cnt == 0 on every link. Within a multi-flow class l_cnt holds the
+  // number of unfrozen members per link, maintained incrementally (members
+  // freeze permanently), which equals the reference's per-round recount; the
+  // rounds then touch only that class's links and its unfrozen members.
   MF_NOINLINE void allocate(int ncls, bool has_caps) {
-    ++s.epoch;
-    if (s.epoch == 0) {  // stamp wrap: reset
-      for (int l = g.lane(); l < I.nlinks; l += G::N) I.l_stamp[l] = 0;
-      g.sync();
-      s.epoch = 1;
-    }
-    // rate-map insertion order for the hash emulation
     const int A = s.n_active;
+    const int RM = I.rmax;
+    // rate-map insertion order for the load_fraction hash emulation
     for (int i = g.lane(); i < A; i += G::N) {
       int fid = I.a_fid[I.s_ord[i]];
       I.h_keys[i] = fid;
@@ -945,140 +1075,132 @@ struct Engine {
       const int o0 = I.s_cls[c], o1 = I.s_cls[c + 1];
       const int n = o1 - o0;
       ++s.classes;
-      if (n == 1) {
+      if (n == 1) {  // singleton: bottleneck residual, capped (allocator.cpp:42-59)
         const int p = I.s_ord[o0];
-        const int fid = I.a_fid[p];
-        const int rb = rbeg(fid), rn = rlen(fid);
+        const int rn = arn(p);
         double r = MF_INF;
         if (has_caps) {
           double cp = I.s_cap[p];
           if (cp < MF_INF) r = smax(0.0, cp);
         }
-        for (int k = 0; k < rn; ++k) r = smin(r, smax(0.0, residual(I.route_links[rb + k])));
+        // lanes gather the route's residuals; min in route order is order-free
+        double mine = MF_INF;
+        if (g.lane() < rn) mine = smax(0.0, I.l_res[arl(p, g.lane())]);
+        for (int k = G::N; k < rn; ++k) mine = smin(mine, smax(0.0, I.l_res[arl(p, k)]));
+        for (int m = G::N / 2; m > 0; m >>= 1) mine = smin(mine, g.shfl_xor(mine, m));
+        r = smin(r, mine);
         g.sync();
-        if (g.leader()) {
-          for (int k = 0; k < rn; ++k) {
-            int l = I.route_links[rb + k];
-            set_residual(l, dsub(residual(l), r));
-          }
-          I.s_rate[p] = r;
+        for (int k = g.lane(); k < rn; k += G::N) {
+          const int l = arl(p, k);
+          I.l_res[l] = dsub(I.l_res[l], r);
         }
+        if (g.leader()) I.s_rate[p] = r;
         g.sync();
         s.algo_bytes += 20LL * rn + 12;
         continue;
       }
-      // multi-flow class: progressive filling rounds
-      for (int i = g.lane(); i < n; i += G::N) {
-        int p = I.s_ord[o0 + i];
-        I.s_rate[p] = 0.0;
-        I.s_frz[p] = 0;
+      // multi-flow class: members start unfrozen at rate 0; count per link
+      int nt = 0;
+      for (int base = 0; base < n; base += G::N) {
+        const int i = base + g.lane();
+        int p = -1, rn = 0;
+        if (i < n) {
+          p = I.s_ord[o0 + i];
+          rn = arn(p);
+          I.s_rate[p] = 0.0;
+          I.s_ul[i] = p;
+        }
+        for (int k = 0; k < RM; ++k) {
+          bool first = false;
+          int l = 0;
+          if (k < rn) {
+            l = arl(p, k);
+            first = g.atomic_add(&I.l_cnt[l], 1) == 0;
+          }
+          const unsigned m = g.ballot(first);
+          if (first) I.s_tl[nt + popc32(m & ((1u << g.lane()) - 1u))] = (unsigned short)l;
+          nt += popc32(m);
+        }
       }
       g.sync();
-      long long guard = (long long)n + I.nlinks + 2;
-      while (guard-- > 0) {
+      int nu = n;
+      while (nu > 0) {
         ++s.rounds;
-        // count unfrozen flows per link; first toucher owns the link
-        bool any = false;
-        for (int i = g.lane(); i < n; i += G::N) {
-          int p = I.s_ord[o0 + i];
-          if (I.s_frz[p]) continue;
-          any = true;
-          int fid = I.a_fid[p];
-          int rb = rbeg(fid), rn = rlen(fid);
-          unsigned own = 0;
-          for (int k = 0; k < rn; ++k) {
-            int old = g.atomic_add(&I.l_cnt[I.route_links[rb + k]], 1);
-            if (old == 0) own |= 1u << k;
-          }
-          I.s_own[p] = (uint8_t)own;
-        }
-        g.sync();
-        if (!g.any(any)) break;
-        // inc = min over touched links and caps
+        // inc = min over touched links of max(0, residual) / count and cap gaps
         double inc = MF_INF;
-        for (int i = g.lane(); i < n; i += G::N) {
-          int p = I.s_ord[o0 + i];
-          if (I.s_frz[p]) continue;
-          int fid = I.a_fid[p];
-          int rb = rbeg(fid), rn = rlen(fid);
-          unsigned own = I.s_own[p];
-          for (int k = 0; k < rn; ++k) {
-            if (!(own & (1u << k))) continue;
-            int l = I.route_links[rb + k];
-            inc = smin(inc, ddiv(smax(0.0, residual(l)), (double)I.l_cnt[l]));
-          }
-          if (has_caps) {
-            double cp = I.s_cap[p];
+        for (int j = g.lane(); j < nt; j += G::N) {
+          const int l = I.s_tl[j];
+          const int cnt = I.l_cnt[l];
+          if (cnt > 0) inc = smin(inc, ddiv(smax(0.0, I.l_res[l]), (double)cnt));
+        }
+        if (has_caps) {
+          for (int i = g.lane(); i < nu; i += G::N) {
+            const int p = I.s_ul[i];
+            const double cp = I.s_cap[p];
             if (cp < MF_INF) inc = smin(inc, dsub(smax(0.0, cp), I.s_rate[p]));
           }
         }
         for (int m = G::N / 2; m > 0; m >>= 1) inc = smin(inc, g.shfl_xor(inc, m));
         inc = smax(inc, 0.0);
-        // apply
-        for (int i = g.lane(); i < n; i += G::N) {
-          int p = I.s_ord[o0 + i];
-          if (I.s_frz[p]) continue;
+        for (int i = g.lane(); i < nu; i += G::N) {
+          const int p = I.s_ul[i];
           I.s_rate[p] = dadd(I.s_rate[p], inc);
-          int fid = I.a_fid[p];
-          int rb = rbeg(fid), rn = rlen(fid);
-          unsigned own = I.s_own[p];
-          for (int k = 0; k < rn; ++k) {
-            if (!(own & (1u << k))) continue;
-            int l = I.route_links[rb + k];
-            set_residual(l, dsub(residual(l), dmul(inc, (double)I.l_cnt[l])));
-          }
+        }
+        for (int j = g.lane(); j < nt; j += G::N) {
+          const int l = I.s_tl[j];
+          const int cnt = I.l_cnt[l];
+          if (cnt > 0) I.l_res[l] = dsub(I.l_res[l], dmul(inc, (double)cnt));
         }
         g.sync();
-        // freeze
+        // freeze at the cap or on a saturated link; compact the unfrozen list
+        int keep_n = 0;
         bool froze = false;
-        for (int i = g.lane(); i < n; i += G::N) {
-          int p = I.s_ord[o0 + i];
-          if (I.s_frz[p]) continue;
-          double cp = MF_INF;
-          if (has_caps) {
-            double c0 = I.s_cap[p];
-            if (c0 < MF_INF) cp = smax(0.0, c0);
-          }
-          double cap_eps = dmul(1e-12, smax(1.0, cp == MF_INF ? 0.0 : cp));
-          bool stop = I.s_rate[p] >= dsub(cp, cap_eps);
-          int fid = I.a_fid[p];
-          int rb = rbeg(fid), rn = rlen(fid);
-          if (!stop) {
-            for (int k = 0; k < rn; ++k) {
-              int l = I.route_links[rb + k];
-              if (residual(l) <= dmul(1e-12, I.cap[l])) {
-                stop = true;
-                break;
-              }
+        for (int base = 0; base < nu; base += G::N) {
+          const int i = base + g.lane();
+          bool keep = false;
+          int p = -1;
+          if (i < nu) {
+            p = I.s_ul[i];
+            double cp = MF_INF;
+            if (has_caps) {
+              const double c0 = I.s_cap[p];
+              if (c0 < MF_INF) cp = smax(0.0, c0);
             }
+            const double cap_eps = dmul(1e-12, smax(1.0, cp == MF_INF ? 0.0 : cp));
+            bool stop = I.s_rate[p] >= dsub(cp, cap_eps);
+            const int rn = arn(p);
+            for (int k = 0; k < rn && !stop; ++k) {
+              const int l = arl(p, k);
+              if (I.l_res[l] <= dmul(1e-12, I.cap[l])) stop = true;
+            }
+            keep = !stop;
+            if (stop)  // a frozen member leaves every link count for good
+              for (int k = 0; k < rn; ++k) g.atomic_add(&I.l_cnt[arl(p, k)], -1);
           }
-          if (stop) {
-            I.s_frz[p] = 2;  // frozen this round (counts still to reset)
-            froze = true;
-          }
+          g.sync();  // every lane has read its entry before the in-place compaction
+          const unsigned m = g.ballot(keep);
+          if (keep) I.s_ul[keep_n + popc32(m & ((1u << g.lane()) - 1u))] = p;
+          keep_n += popc32(m);
+          if (i < nu && !keep) froze = true;
         }
         g.sync();
-        // reset counts of the links touched this round
-        for (int i = g.lane(); i < n; i += G::N) {
-          int p = I.s_ord[o0 + i];
-          int fz = I.s_frz[p];
-          if (fz == 1) continue;
-          int fid = I.a_fid[p];
-          int rb = rbeg(fid);
-          unsigned own = I.s_own[p];
-          for (int k = 0; own; ++k, own >>= 1)
-            if (own & 1u) I.l_cnt[I.route_links[rb + k]] = 0;
-          I.s_own[p] = 0;
-          if (fz == 2) I.s_frz[p] = 1;
-        }
-        g.sync();
-        s.algo_bytes += (long long)n * (20LL * I.rmax + 29);
+        s.algo_bytes += (long long)nu * (20LL * RM + 29) + 32LL * nt;
         if (!g.any(froze)) {
           fail(ERR_INTERNAL, CHK_NO_PROGRESS);
           return;
         }
+        nu = keep_n;
       }
     }
+    // restore l_res == capacity on every link a route of this step touched
+    for (int p = g.lane(); p < A; p += G::N) {
+      const int rn = arn(p);
+      for (int k = 0; k < rn; ++k) {
+        const int l = arl(p, k);
+        I.l_res[l] = I.cap[l];
+      }
+    }
+    g.sync();
   }
 
   // engine.cpp:278-293
@@ -1122,7 +1244,7 @@ struct Engine {
   }
 
   // ===================================================== K1: stage DAG
-  MF_FN bool layer_deps_met(int b, int layer) const {  // engine.cpp:356-369
+  MF_FN bool layer_deps_met(int b, int layer) {  // engine.cpp:356-369
     const int base = I.b_lbase[b];
     const int idx = layer - 1;
     if (layer > 1) {
@@ -1131,42 +1253,40 @@ struct Engine {
       if (c >= 0 && I.c_open[c] > 0) return false;
     }
     const int ro = I.pl_roff[base + idx], rc = I.pl_rcnt[base + idx];
-    for (int k = 0; k < rc; ++k) {
+    bool blocked = false;
+    for (int k = g.lane(); k < rc; k += G::N) {
       int fid = I.rpool[ro + k];
       int r = I.f_req[fid];
-      if (r >= 0 && I.r_pruned[r]) continue;
-      if (!done(fid)) return false;
+      if (r >= 0 && I.r_pruned[r]) continue;  // waived
+      if (!done(fid)) blocked = true;
     }
-    return true;
+    return !g.any(blocked);
   }
 
   MF_FN void try_start_layers(int b) {  // engine.cpp:371-382
     const int L = I.b_layers[b];
     const int base = I.b_lbase[b];
-    for (int layer = 1; layer <= L; ++layer) {
-      const int idx = base + layer - 1;
-      if (I.pl_started[idx]) continue;
-      if (!layer_deps_met(b, layer)) return;
-      g.sync();
-      if (g.leader()) {
-        I.pl_started[idx] = 1;
-        I.pl_start[idx] = s.now;
-      }
-      g.sync();
-      push(dadd(s.now, I.pl_cost[idx]), EV_COMPUTE, b, layer);
-      return;
+    // first layer not yet started; only it may start (one layer at a time)
+    int layer = 0;
+    for (int l0 = 0; l0 < L && !layer; l0 += G::N) {
+      const int l = l0 + g.lane();
+      const unsigned m = g.ballot(l < L && !I.pl_started[base + l]);
+      if (m) layer = l0 + ctz32(m) + 1;
     }
+    if (!layer || !layer_deps_met(b, layer)) return;
+    const int idx = base + layer - 1;
+    g.sync();
+    if (g.leader()) {
+      I.pl_started[idx] = 1;
+      I.pl_start[idx] = s.now;
+    }
+    g.sync();
+    push(dadd(s.now, I.pl_cost[idx]), EV_COMPUTE, b, layer);
   }
 
   MF_FN void check_pipeline_done(int b) {  // engine.cpp:384-393
     if (I.b_done[b] != kNoTime) return;
-    const int L = I.b_layers[b];
-    const int base = I.b_lbase[b];
-    for (int i = 0; i < L; ++i) {
-      if (!I.pl_done[base + i]) return;
-      int c = I.pl_coll[base + i];
-      if (c >= 0 && I.c_open[c] > 0) return;
-    }
+    if (!pipeline_complete(b)) return;
     put(&I.b_done[b], s.now);
     push(s.now, EV_DEPART, b, -1);
   }
@@ -1251,6 +1371,10 @@ struct Engine {
     if (s.err) return;
     const int c = I.f_cof[fid];
     if (c >= 0 && I.c_rel[c] == kNoTime) put(&I.c_rel[c], s.now);
+    if (I.f_size[fid] > 0.0 && I.f_route[fid] < 0) {
+      fail(ERR_SIM, CHK_ROUTE);
+      return;
+    }
     if (I.f_size[fid] <= 0.0 || rlen(fid) == 0) {
       finish_flow(fid);
       return;
@@ -1260,6 +1384,11 @@ struct Engine {
       return;
     }
     const int pos = s.n_active;
+    const int rb = rbeg(fid), rn = rlen(fid);
+    if (rn > I.rmax) {
+      fail(ERR_INTERNAL, CHK_ROUTE);
+      return;
+    }
     g.sync();
     if (g.leader()) {
       I.a_fid[pos] = fid;
@@ -1267,7 +1396,18 @@ struct Engine {
       I.a_rate[pos] = 0.0;
       I.a_evt[pos] = 0.0;
       I.a_evseq[pos] = kNoSeq;
+      I.a_rn[pos] = (uint8_t)rn;
       I.f_apos[fid] = pos;
+    }
+    for (int k = g.lane(); k < rn; k += G::N)
+      I.a_rl[pos * I.rmax + k] = (unsigned short)I.route_links[rb + k];
+    if (I.p.policy != POL_FS && s.n_add >= 0) {
+      if (s.n_add < I.A_cap) {
+        if (g.leader()) I.srt_add[s.n_add] = fid;
+        ++s.n_add;
+      } else {
+        s.n_add = -1;  // too many to merge: rebuild the order from scratch
+      }
     }
     g.sync();
     ++s.n_active;
@@ -1962,7 +2102,7 @@ struct Engine {
       I.q_tail[u] = 0;
     }
     for (int l = g.lane(); l < I.nlinks; l += G::N) {
-      I.l_stamp[l] = 0;
+      I.l_res[l] = I.cap[l];
       I.l_cnt[l] = 0;
     }
     g.sync();
@@ -1993,11 +2133,13 @@ struct Engine {
     s.pruned = 0;
     s.max_active = 0;
     s.horizon = I.p.horizon;
+    s.n_srt = 0;
+    s.n_add = 0;
     if (!I.host_init) {
       init_state();
     } else {
       for (int l = g.lane(); l < I.nlinks; l += G::N) {
-        I.l_stamp[l] = 0;
+        I.l_res[l] = I.cap[l];
         I.l_cnt[l] = 0;
       }
       g.sync();
@@ -2029,6 +2171,10 @@ struct Engine {
       }
       advance_to(e.t);
       if (s.err) break;
+#if defined(MF_TRACE) && !defined(__CUDACC__)
+      fprintf(stderr, "ev %lld t=%.17g kind=%d a=%d b=%d nact=%d nev=%d\n", s.events, e.t, kind, a, b,
+              s.n_active, s.n_ev);
+#endif
       ++s.events;
       if (e.t == s.prev_t) {
         if (++s.streak > I.p.livelock) {

@@ -16,18 +16,104 @@
 
 namespace mfb {
 
-constexpr int kWarpsPerBlock = 4;
+// Per-warp shared-memory plan of one launch: the descriptor copy, then the
+// hot arrays of an instance whenever its capacities fit (active-flow state +
+// route cache + per-step rates, the event pool, per-link residual / count).
+struct SmemPlan {
+  int AS;  // active flows
+  int RM;  // route length stride
+  int ES;  // event pool
+  int NL;  // links
+  int bytes;
+};
 
-__global__ void __launch_bounds__(32 * kWarpsPerBlock)
-    mfsim_engine_kernel(const Inst* __restrict__ insts, int n, int* __restrict__ next) {
+__host__ __device__ inline int align16(int x) { return (x + 15) & ~15; }
+
+__host__ inline SmemPlan make_plan(int rmax, int nlinks) {
+  SmemPlan p{};
+  p.AS = mfh::kSmemActive;
+  p.RM = rmax;
+  p.ES = mfh::kSmemEvents;
+  p.NL = nlinks <= mfh::kSmemLinks ? nlinks : 0;
+  int b = align16(sizeof(Inst));
+  b += align16(p.AS * 4) + 4 * align16(p.AS * 8) + align16(p.AS * p.RM * 2) + align16(p.AS);
+  b += align16(p.AS * 8) + align16(p.AS * 4);                       // s_rate, s_ul
+  b += align16(p.ES * 8) * 2 + align16(p.ES * 4) * 3;               // event pool
+  b += align16(p.NL * 8) + align16(p.NL * 4) + align16(p.NL * 2);   // l_res, l_cnt, s_tl
+  p.bytes = align16(b);
+  return p;
+}
+
+__global__ void __launch_bounds__(32)
+    mfsim_engine_kernel(const Inst* __restrict__ insts, int n, int* __restrict__ next,
+                        SmemPlan plan) {
+  extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31;
+  Inst* d = reinterpret_cast<Inst*>(smem);
   for (;;) {
     int i = 0;
     if (lane == 0) i = atomicAdd(next, 1);
     i = __shfl_sync(0xffffffffu, i, 0);
     if (i >= n) return;
-    Engine<WarpLanes> eng(insts[i]);
+    // descriptor copy (8-byte words across the warp)
+    {
+      const unsigned long long* src = reinterpret_cast<const unsigned long long*>(insts + i);
+      unsigned long long* dst = reinterpret_cast<unsigned long long*>(d);
+      for (int w = lane; w < (int)(sizeof(Inst) / 8); w += 32) dst[w] = src[w];
+    }
+    __syncwarp();
+    if (lane == 0) {
+      unsigned char* q = smem + align16(sizeof(Inst));
+      auto take = [&](int bytes) {
+        unsigned char* r = q;
+        q += align16(bytes);
+        return r;
+      };
+      if (d->A_cap <= plan.AS && d->rmax <= plan.RM) {
+        d->a_fid = reinterpret_cast<int*>(take(plan.AS * 4));
+        d->a_rem = reinterpret_cast<double*>(take(plan.AS * 8));
+        d->a_rate = reinterpret_cast<double*>(take(plan.AS * 8));
+        d->a_evt = reinterpret_cast<double*>(take(plan.AS * 8));
+        d->a_evseq = reinterpret_cast<unsigned long long*>(take(plan.AS * 8));
+        d->a_rl = reinterpret_cast<unsigned short*>(take(plan.AS * plan.RM * 2));
+        d->a_rn = reinterpret_cast<uint8_t*>(take(plan.AS));
+        d->s_rate = reinterpret_cast<double*>(take(plan.AS * 8));
+        d->s_ul = reinterpret_cast<int*>(take(plan.AS * 4));
+      } else {
+        q += align16(plan.AS * 4) + 4 * align16(plan.AS * 8) + align16(plan.AS * plan.RM * 2) +
+             align16(plan.AS) + align16(plan.AS * 8) + align16(plan.AS * 4);
+      }
+      if (d->E_cap <= plan.ES) {
+        double* et = reinterpret_cast<double*>(take(plan.ES * 8));
+        unsigned long long* es = reinterpret_cast<unsigned long long*>(take(plan.ES * 8));
+        int* ek = reinterpret_cast<int*>(take(plan.ES * 4));
+        int* ea = reinterpret_cast<int*>(take(plan.ES * 4));
+        int* eb = reinterpret_cast<int*>(take(plan.ES * 4));
+        for (int e = 0; e < d->n_ev0; ++e) {  // host-prepared initial events
+          et[e] = d->e_t[e];
+          es[e] = d->e_seq[e];
+          ek[e] = d->e_kind[e];
+          ea[e] = d->e_a[e];
+          eb[e] = d->e_b[e];
+        }
+        d->e_t = et;
+        d->e_seq = es;
+        d->e_kind = ek;
+        d->e_a = ea;
+        d->e_b = eb;
+      } else {
+        q += 2 * align16(plan.ES * 8) + 3 * align16(plan.ES * 4);
+      }
+      if (plan.NL > 0 && d->nlinks <= plan.NL) {
+        d->l_res = reinterpret_cast<double*>(take(plan.NL * 8));
+        d->l_cnt = reinterpret_cast<int*>(take(plan.NL * 4));
+        d->s_tl = reinterpret_cast<unsigned short*>(take(plan.NL * 2));
+      }
+    }
+    __syncwarp();
+    Engine<WarpLanes> eng(*d);
     eng.run();
+    __syncwarp();
   }
 }
 
@@ -50,16 +136,12 @@ class CudaBackend final : public Backend {
     ck(cudaEventCreate(&e0_), "cudaEventCreate");
     ck(cudaEventCreate(&e1_), "cudaEventCreate");
     ck(cudaMalloc(&counter_, sizeof(int)), "cudaMalloc counter");
-    int sms = 0;
-    ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device), "attr");
-    int per_sm = 0;
-    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mfb::mfsim_engine_kernel,
-                                                     32 * mfb::kWarpsPerBlock, 0),
-       "occupancy");
-    if (per_sm < 1) per_sm = 1;
-    grid_ = sms * per_sm;
+    ck(cudaDeviceGetAttribute(&sms_, cudaDevAttrMultiProcessorCount, device), "attr");
+    ck(cudaFuncSetAttribute(mfb::mfsim_engine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            200 * 1024),
+       "smem attr");
     // deep per-warp call chains (noinline handlers) need more than the default
-    ck(cudaDeviceSetLimit(cudaLimitStackSize, 16384), "stack limit");
+    ck(cudaDeviceSetLimit(cudaLimitStackSize, 4096), "stack limit");
   }
   ~CudaBackend() override {
     cudaFree(counter_);
@@ -86,17 +168,23 @@ class CudaBackend final : public Backend {
   void d2h(void* h, const void* d, size_t n) override {
     if (n) ck(cudaMemcpyAsync(h, d, n, cudaMemcpyDeviceToHost, stream_), "D2H");
   }
-  void launch(const mfb::Inst* d, int n) override {
+  void launch(const mfb::Inst* d, int n, const LaunchHint& hint) override {
+    const mfb::SmemPlan plan = mfb::make_plan(hint.rmax, hint.nlinks);
+    int per_sm = 0;
+    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mfb::mfsim_engine_kernel, 32,
+                                                     plan.bytes),
+       "occupancy");
+    if (per_sm < 1) per_sm = 1;
+    int grid = sms_ * per_sm;
+    if (n < grid) grid = n > 0 ? n : 1;
     ck(cudaMemsetAsync(counter_, 0, sizeof(int), stream_), "memset");
-    int grid = grid_;
-    const int warps_needed = (n + mfb::kWarpsPerBlock - 1) / mfb::kWarpsPerBlock;
-    if (warps_needed < grid) grid = warps_needed > 0 ? warps_needed : 1;
     ck(cudaEventRecord(e0_, stream_), "event");
-    mfb::mfsim_engine_kernel<<<grid, 32 * mfb::kWarpsPerBlock, 0, stream_>>>(d, n, counter_);
+    mfb::mfsim_engine_kernel<<<grid, 32, plan.bytes, stream_>>>(d, n, counter_, plan);
     ck(cudaGetLastError(), "launch");
     ck(cudaEventRecord(e1_, stream_), "event");
     ++launches_;
     timed_ = true;
+    last_grid_ = grid;
   }
   void sync() override {
     ck(cudaStreamSynchronize(stream_), "kernel");
@@ -115,7 +203,8 @@ class CudaBackend final : public Backend {
   cudaStream_t own_ = nullptr, stream_ = nullptr;
   cudaEvent_t e0_ = nullptr, e1_ = nullptr;
   int* counter_ = nullptr;
-  int grid_ = 148;
+  int sms_ = 148;
+  int last_grid_ = 0;
   int launches_ = 0;
   bool timed_ = false;
   double last_ms_ = 0.0;

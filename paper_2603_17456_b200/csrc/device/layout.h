@@ -151,6 +151,8 @@ struct Inst {
   double* a_rate;
   double* a_evt;
   unsigned long long* a_evseq;  // ~0 = no pending completion event
+  unsigned short* a_rl;         // route link ids, rmax per active flow
+  uint8_t* a_rn;                // route length
   // ---- batches [B_cap]
   int* b_unit;
   int* b_layers;
@@ -194,9 +196,8 @@ struct Inst {
   int* e_a;
   int* e_b;
   // ---- links [nlinks]
-  double* l_res;
-  unsigned* l_stamp;
-  int* l_cnt;
+  double* l_res;   // == capacity outside allocate()
+  int* l_cnt;      // == 0 outside a multi-flow class
   double* l_x;  // scratch (Karuna demand / Algorithm 1 S)
   double* l_y;  // scratch (Algorithm 1 L)
   // ---- per-step scratch [A_cap] / [X_cap = A_cap * rmax]
@@ -204,8 +205,10 @@ struct Inst {
   double* s_cap;    // caps by active position (+inf none)
   int* s_ord;       // class order (active positions)
   int* s_cls;       // class start offsets (+1 sentinel)
-  uint8_t* s_frz;   // frozen flag
-  uint8_t* s_own;   // owned-link mask this round
+  int* s_ul;        // unfrozen members of the class being filled
+  unsigned short* s_tl;  // links touched by that class [nlinks]
+  int* srt;         // sorted-subset order of the last decide (flow ids)
+  int* srt_add;     // flows released since the last decide
   unsigned long long* s_k0;
   unsigned long long* s_k1;
   unsigned long long* s_k2;

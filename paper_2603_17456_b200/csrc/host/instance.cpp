@@ -490,7 +490,7 @@ void carve_instance(Carver& c, const InstanceInput& in, Inst& d, const Inst& top
     PL = B * L;
     RP = PP = n_req * L;
     CM = coll ? B * L * per : 1;
-    E = 2 * n_req + 4L * units + 64 + in.e_boost;
+    E = in.e_boost > 0 ? 2 * n_req + 4L * units + 64 + in.e_boost : kSmemEvents;
     MP = n_req;
   } else {
     n_req = static_cast<long>(m->r_arrival.size());
@@ -508,7 +508,7 @@ void carve_instance(Carver& c, const InstanceInput& in, Inst& d, const Inst& top
     for (auto& cf : m->coflows) CM += static_cast<long>(cf.members.size());
     E = B * 3 + F + 64 + in.e_boost;
   }
-  A = in.a_cap > 0 ? in.a_cap : std::min<long>(std::max<long>(F, 1), 4096);
+  A = in.a_cap > 0 ? in.a_cap : std::min<long>(std::max<long>(F, 1), kSmemActive);
   A = std::max<long>(A, 1);
   const long X = A * d.rmax;
   const int LR = t.lr_cap;
@@ -623,6 +623,8 @@ void carve_instance(Carver& c, const InstanceInput& in, Inst& d, const Inst& top
   d.a_rate = c.S<double>(nA);
   d.a_evt = c.S<double>(nA);
   d.a_evseq = c.S<unsigned long long>(nA);
+  d.a_rl = c.S<unsigned short>(nA * d.rmax);
+  d.a_rn = c.S<uint8_t>(nA);
   d.b_unit = state((int*)nullptr, nB);
   d.b_layers = state((int*)nullptr, nB);
   d.b_lbase = state((int*)nullptr, nB);
@@ -663,7 +665,6 @@ void carve_instance(Carver& c, const InstanceInput& in, Inst& d, const Inst& top
   d.e_b = state((int*)nullptr, d.E_cap);
   const size_t nl = std::max(d.nlinks, 1);
   d.l_res = c.S<double>(nl);
-  d.l_stamp = c.S<unsigned>(nl);
   d.l_cnt = c.S<int>(nl);
   d.l_x = c.S<double>(nl);
   d.l_y = c.S<double>(nl);
@@ -672,8 +673,10 @@ void carve_instance(Carver& c, const InstanceInput& in, Inst& d, const Inst& top
   d.s_cap = c.S<double>(nA);
   d.s_ord = c.S<int>(2 * pA);
   d.s_cls = c.S<int>(nA + 1);
-  d.s_frz = c.S<uint8_t>(nA);
-  d.s_own = c.S<uint8_t>(nA);
+  d.s_ul = c.S<int>(nA);
+  d.s_tl = c.S<unsigned short>(nl);
+  d.srt = c.S<int>(nA);
+  d.srt_add = c.S<int>(nA);
   d.s_k0 = c.S<unsigned long long>(nA);
   d.s_k1 = c.S<unsigned long long>(nA);
   d.s_k2 = c.S<unsigned long long>(nA);
@@ -852,6 +855,11 @@ void Batch::pack() {
                      &ov.rbatch);
     }
     if (!c.real) {
+      hint_ = LaunchHint{};
+      for (const Inst& d : desc_) {
+        hint_.rmax = std::max(hint_.rmax, d.rmax);
+        hint_.nlinks = std::max(hint_.nlinks, d.nlinks);
+      }
       in_bytes_ = c.in.off;
       st_bytes_ = c.st.off;
       out_bytes_ = c.out.off;
@@ -870,7 +878,7 @@ void Batch::upload() {
   be_.h2d(desc_dev_, desc_.data(), sizeof(Inst) * desc_.size());
 }
 
-void Batch::launch() { be_.launch(desc_dev_, size()); }
+void Batch::launch() { be_.launch(desc_dev_, size(), hint_); }
 
 size_t Batch::output_bytes(int detail) const {
   size_t b = out_bytes_;

@@ -20,6 +20,18 @@
 
 namespace mfh {
 
+// First-attempt capacities; they match the per-warp shared-memory plan of the
+// kernel, so instances that stay within them run with their hot state on chip.
+// An instance that outgrows one is re-run with a larger, global-memory bound.
+constexpr int kSmemActive = 256;
+constexpr int kSmemEvents = 128;
+constexpr int kSmemLinks = 1024;
+
+struct LaunchHint {
+  int rmax = 1;    // longest route of any instance
+  int nlinks = 1;  // most links of any instance
+};
+
 // Device execution backend: the product build links the CUDA backend only.
 class Backend {
  public:
@@ -31,7 +43,7 @@ class Backend {
   virtual void host_free(void* p) = 0;
   virtual void h2d(void* dst, const void* src, size_t n) = 0;  // stream-ordered
   virtual void d2h(void* dst, const void* src, size_t n) = 0;
-  virtual void launch(const mfb::Inst* d_insts, int n) = 0;
+  virtual void launch(const mfb::Inst* d_insts, int n, const LaunchHint& hint) = 0;
   virtual void sync() = 0;
   virtual void set_stream(void* stream) = 0;
   virtual double last_kernel_ms() const = 0;
@@ -127,6 +139,7 @@ class Batch {
   char* st_dev_ = nullptr;
   char* out_dev_ = nullptr;
   mfb::Inst* desc_dev_ = nullptr;
+  LaunchHint hint_;
   size_t in_bytes_ = 0, st_bytes_ = 0, out_bytes_ = 0;
   struct OutView {
     size_t out, ttft, pruned, stall, rbatch;
