@@ -353,78 +353,130 @@ struct Engine {
     return I.p.K;
   }
 
+  // Stable bucketing by link of n entries (link x_seg[e], key x_hi[e], value
+  // x_val[e]) into y_key / y_val: a warp counting sort whose scatter ranks
+  // equal links by lane (match_any), so each link's bucket keeps entry order.
+  // On return l_cnt[l] = bucket size, l_off[l] = bucket end for the touched
+  // links s_tl[0, nt); release() must zero l_cnt again.
+  MF_FN int bucket_by_link(int n) {
+    int nt = 0;
+    for (int base = 0; base < n; base += G::N) {
+      const int e = base + g.lane();
+      bool first = false;
+      int l = 0;
+      if (e < n) {
+        l = I.x_seg[e];
+        first = g.atomic_add(&I.l_cnt[l], 1) == 0;
+      }
+      const unsigned m = g.ballot(first);
+      if (first) I.s_tl[nt + popc32(m & g.lanemask_lt())] = (unsigned short)l;
+      nt += popc32(m);
+    }
+    g.sync();
+    int off = 0;
+    for (int base = 0; base < nt; base += G::N) {
+      const int j = base + g.lane();
+      int c = 0, l = 0;
+      if (j < nt) {
+        l = I.s_tl[j];
+        c = I.l_cnt[l];
+      }
+      int tot;
+      const int o = g.excl_scan(c, &tot);
+      if (j < nt) I.l_off[l] = off + o;
+      off += tot;
+    }
+    g.sync();
+    for (int base = 0; base < n; base += G::N) {
+      const int e = base + g.lane();
+      const int l = e < n ? I.x_seg[e] : -1 - g.lane();
+      const unsigned peers = g.match_any(l);
+      if (e < n) {
+        const int pos = I.l_off[l] + popc32(peers & g.lanemask_lt());
+        I.y_key[pos] = I.x_hi[e];
+        I.y_val[pos] = I.x_val[e];
+      }
+      g.sync();
+      if (e < n && (peers >> g.lane()) == 1u) I.l_off[l] += popc32(peers);
+      g.sync();
+    }
+    return nt;
+  }
+  MF_FN void bucket_release(int nt) {
+    for (int j = g.lane(); j < nt; j += G::N) I.l_cnt[I.s_tl[j]] = 0;
+    g.sync();
+  }
+
   // LinkLoadIndex (allocator.cpp:143-161): entries (link, band<<16|level, rate)
-  // for allocated flows with rate > 0, sorted, prefix sums per link.
+  // for allocated flows with rate > 0; per link sorted by (key, rate) with
+  // running sums. Returns the touched-link count (see index_release).
   MF_NOINLINE int build_index() {
-    // count entries
-    int total = 0;
+    int n = 0;
     for (int base = 0; base < s.n_active; base += G::N) {
-      int p = base + g.lane();
+      const int p = base + g.lane();
       int c = 0;
       if (p < s.n_active && I.a_rate[p] > 0.0) c = arn(p);
       int tot;
-      int off = g.excl_scan(c, &tot);
+      const int off = g.excl_scan(c, &tot);
       if (c > 0) {
-        int fid = I.a_fid[p];
-        unsigned long long key = ((unsigned long long)I.f_band[fid] << 16) | I.f_level[fid];
-        double r = I.a_rate[p];
+        const int fid = I.a_fid[p];
+        const unsigned long long key = ((unsigned long long)I.f_band[fid] << 16) | I.f_level[fid];
+        const double r = I.a_rate[p];
         for (int k = 0; k < c; ++k) {
-          int l = arl(p, k);
-          I.x_hi[total + off + k] = ((unsigned long long)l << 32) | key;
-          I.x_lo[total + off + k] = dbits(r);
-          I.x_val[total + off + k] = r;
+          I.x_seg[n + off + k] = arl(p, k);
+          I.x_hi[n + off + k] = key;
+          I.x_val[n + off + k] = r;
         }
       }
-      total += tot;
+      n += tot;
     }
     g.sync();
-    if (total > I.X_cap) {
+    if (n > I.X_cap) {
       fail(ERR_INTERNAL, CHK_CAP_SCRATCH);
       return 0;
     }
-    sort_x(total);
-    // segment heads -> sequential prefix sums per link segment
-    int nseg = 0;
-    for (int base = 0; base < total; base += G::N) {
-      int i = base + g.lane();
-      int h = 0;
-      if (i < total) h = (i == 0 || (I.x_hi[i] >> 32) != (I.x_hi[i - 1] >> 32)) ? 1 : 0;
-      int tot;
-      int off = g.excl_scan(h, &tot);
-      if (h) I.x_seg[nseg + off] = i;
-      nseg += tot;
-    }
-    g.sync();
-    for (int k = g.lane(); k < nseg; k += G::N) {
-      int i0 = I.x_seg[k];
-      int i1 = (k + 1 < nseg) ? I.x_seg[k + 1] : total;
+    const int nt = bucket_by_link(n);
+    // per link: insertion sort by (key, rate), then running sums in that order
+    for (int j = g.lane(); j < nt; j += G::N) {
+      const int l = I.s_tl[j];
+      const int e1 = I.l_off[l], e0 = e1 - I.l_cnt[l];
+      for (int a = e0 + 1; a < e1; ++a) {
+        const unsigned long long k = I.y_key[a];
+        const double v = I.y_val[a];
+        const unsigned long long vb = dbits(v);
+        int m = a;
+        while (m > e0 && (I.y_key[m - 1] > k || (I.y_key[m - 1] == k && dbits(I.y_val[m - 1]) > vb))) {
+          I.y_key[m] = I.y_key[m - 1];
+          I.y_val[m] = I.y_val[m - 1];
+          --m;
+        }
+        I.y_key[m] = k;
+        I.y_val[m] = v;
+      }
       double run = 0.0;
-      for (int i = i0; i < i1; ++i) {
-        run = dadd(run, I.x_val[i]);
-        I.x_pre[i] = run;
+      for (int a = e0; a < e1; ++a) {
+        run = dadd(run, I.y_val[a]);
+        I.x_pre[a] = run;
       }
     }
     g.sync();
-    s.algo_bytes += 40LL * total;
-    return total;
+    s.algo_bytes += 40LL * n;
+    return nt;
   }
 
   // LinkLoadIndex::higher_fraction (allocator.cpp:163-171); per-lane query
-  MF_FN double index_fraction(int nx, int l, int band, int level) const {
-    unsigned long long want = ((unsigned long long)l << 32) |
-                              (((unsigned long long)band << 16) | (unsigned long long)level);
-    // first entry with hi >= want
-    int lo = 0, hi = nx;
+  MF_FN double index_fraction(int l, int band, int level) const {
+    const int cnt = I.l_cnt[l];
+    if (cnt == 0) return 0.0;
+    const unsigned long long want = ((unsigned long long)band << 16) | (unsigned long long)level;
+    const int e1 = I.l_off[l], e0 = e1 - cnt;
+    int lo = e0, hi = e1;  // first entry with key >= want
     while (lo < hi) {
-      int mid = (lo + hi) >> 1;
-      if (I.x_hi[mid] < want)
-        lo = mid + 1;
-      else
-        hi = mid;
+      const int mid = (lo + hi) >> 1;
+      if (I.y_key[mid] < want) lo = mid + 1; else hi = mid;
     }
-    if (lo == 0 || (I.x_hi[lo - 1] >> 32) != (unsigned long long)l) return 0.0;
-    double load = I.x_pre[lo - 1];
-    double v = ddiv(load, I.cap[l]);
+    if (lo == e0) return 0.0;
+    const double v = ddiv(I.x_pre[lo - 1], I.cap[l]);
     return v < 0.0 ? 0.0 : (1.0 < v ? 1.0 : v);
   }
 
@@ -560,7 +612,7 @@ struct Engine {
       double best_eff = MF_INF;
       for (int k = 0; k < rn; ++k) {
         int l = I.route_links[rb + k];
-        double rho = use_idx ? index_fraction(nx, l, pb, pl) : load_fraction(l, pb, pl);
+        double rho = use_idx ? index_fraction(l, pb, pl) : load_fraction(l, pb, pl);
         double eff = dmul(I.cap[l], dsub(1.0, rho));
         if (eff < best_eff) best_eff = eff;
       }
@@ -655,6 +707,7 @@ struct Engine {
       changed = true;
     }
     g.sync();
+    bucket_release(nx);
     s.algo_bytes += 40LL * fc;
     if (g.any(bad)) fail(ERR_INTERNAL, CHK_NEG_MLU);
     if (g.any(urgent_bad)) fail(ERR_INTERNAL, CHK_URGENT_BAND);
@@ -967,85 +1020,61 @@ struct Engine {
   }
 
   // Karuna caps for the deadline class s_ord[0, nd): per-link demand summed in
-  // active order (baselines.cpp:102-133).
+  // active order (baselines.cpp:102-133), via stable bucketing by link.
   MF_NOINLINE void karuna_caps(int nd) {
     const int A = s.n_active;
     for (int p = g.lane(); p < A; p += G::N) I.s_cap[p] = MF_INF;
     g.sync();
-    // entries (link, active position) for flows with a positive slack
-    int total = 0;
+    int n = 0;
     for (int base = 0; base < nd; base += G::N) {
-      int i = base + g.lane();
-      int c = 0;
-      int p = -1, fid = -1;
+      const int i = base + g.lane();
+      int c = 0, p = -1;
       double want = 0.0;
       if (i < nd) {
         p = I.s_ord[i];
-        fid = I.a_fid[p];
-        double slack = dsub(I.f_dl[fid], s.now);
+        const double slack = dsub(I.f_dl[I.a_fid[p]], s.now);
         if (slack > 0.0) {
           want = ddiv(I.a_rem[p], slack);
           c = arn(p);
         }
       }
       int tot;
-      int off = g.excl_scan(c, &tot);
+      const int off = g.excl_scan(c, &tot);
       if (c > 0) {
         for (int k = 0; k < c; ++k) {
-          int l = arl(p, k);
-          I.x_hi[total + off + k] = ((unsigned long long)l << 32) | (unsigned)p;
-          I.x_lo[total + off + k] = 0;
-          I.x_val[total + off + k] = want;
+          I.x_seg[n + off + k] = arl(p, k);
+          I.x_hi[n + off + k] = 0;
+          I.x_val[n + off + k] = want;
         }
-        I.s_rate[p] = want;  // stash want
+        I.s_cap[p] = want;  // stash: capped below
       }
-      total += tot;
+      n += tot;
     }
     g.sync();
-    if (total > I.X_cap) {
+    if (n > I.X_cap) {
       fail(ERR_INTERNAL, CHK_CAP_SCRATCH);
       return;
     }
-    // order by (link, active position) -> demand per link in active order
-    for (int i = g.lane(); i < total; i += G::N) {
-      unsigned long long hi = I.x_hi[i];
-      unsigned p = (unsigned)(hi & 0xffffffffu);
-      I.x_lo[i] = p;
-      I.x_hi[i] = hi >> 32;
+    const int nt = bucket_by_link(n);
+    for (int j = g.lane(); j < nt; j += G::N) {
+      const int l = I.s_tl[j];
+      const int e1 = I.l_off[l], e0 = e1 - I.l_cnt[l];
+      double dmd = 0.0;
+      for (int a = e0; a < e1; ++a) dmd = dadd(dmd, I.y_val[a]);
+      I.l_x[l] = dmd;
     }
     g.sync();
-    sort_x(total);
-    int nseg = 0;
-    for (int base = 0; base < total; base += G::N) {
-      int i = base + g.lane();
-      int h = 0;
-      if (i < total) h = (i == 0 || I.x_hi[i] != I.x_hi[i - 1]) ? 1 : 0;
-      int tot;
-      int off = g.excl_scan(h, &tot);
-      if (h) I.x_seg[nseg + off] = i;
-      nseg += tot;
-    }
-    g.sync();
-    for (int k = g.lane(); k < nseg; k += G::N) {
-      int i0 = I.x_seg[k];
-      int i1 = (k + 1 < nseg) ? I.x_seg[k + 1] : total;
-      double d = 0.0;
-      for (int i = i0; i < i1; ++i) d = dadd(d, I.x_val[i]);
-      I.l_x[(int)I.x_hi[i0]] = d;
-    }
-    g.sync();
+    bucket_release(nt);
     for (int i = g.lane(); i < nd; i += G::N) {
-      int p = I.s_ord[i];
-      int fid = I.a_fid[p];
-      double slack = dsub(I.f_dl[fid], s.now);
-      if (!(slack > 0.0)) continue;
-      double want = I.s_rate[p];
+      const int p = I.s_ord[i];
+      const double want = I.s_cap[p];
+      if (!(want < MF_INF)) continue;  // no positive slack: uncapped
       double scale = 1.0;
       const int rn = arn(p);
       for (int k = 0; k < rn; ++k) {
-        int l = arl(p, k);
-        double c = I.cap[l];
-        double dmd = I.l_x[l];
+        const int l = arl(p, k);
+        const double c = I.cap[l];
+        const double dmd = I.l_x[l];
         if (dmd > c) scale = smin(scale, ddiv(c, dmd));
       }
       I.s_cap[p] = dmul(want, scale);

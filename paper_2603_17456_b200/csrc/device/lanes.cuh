@@ -50,6 +50,8 @@ struct WarpLanes {
   MF_FN int shfl_up(int v, int d) const { return __shfl_up_sync(0xffffffffu, v, d); }
   MF_FN unsigned ballot(bool p) const { return __ballot_sync(0xffffffffu, p); }
   MF_FN bool any(bool p) const { return __any_sync(0xffffffffu, p); }
+  MF_FN unsigned match_any(int v) const { return __match_any_sync(0xffffffffu, v); }
+  MF_FN unsigned lanemask_lt() const { return (1u << (threadIdx.x & 31)) - 1u; }
   MF_FN int sum(int v) const { return __reduce_add_sync(0xffffffffu, (unsigned)v); }
   MF_FN int atomic_add(int* p, int v) const { return atomicAdd(p, v); }
   MF_FN unsigned atomic_or(unsigned* p, unsigned v) const { return atomicOr(p, v); }
@@ -82,6 +84,8 @@ struct SerialLanes {
   inline int shfl_up(int v, int) const { return v; }
   inline unsigned ballot(bool p) const { return p ? 1u : 0u; }
   inline bool any(bool p) const { return p; }
+  inline unsigned match_any(int) const { return 1u; }
+  inline unsigned lanemask_lt() const { return 0u; }
   inline int sum(int v) const { return v; }
   inline int atomic_add(int* p, int v) const {
     int o = *p;

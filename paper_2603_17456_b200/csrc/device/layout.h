@@ -198,6 +198,7 @@ struct Inst {
   // ---- links [nlinks]
   double* l_res;   // == capacity outside allocate()
   int* l_cnt;      // == 0 outside a multi-flow class
+  int* l_off;   // bucket cursor / end offset while entries are bucketed by link
   double* l_x;  // scratch (Karuna demand / Algorithm 1 S)
   double* l_y;  // scratch (Algorithm 1 L)
   // ---- per-step scratch [A_cap] / [X_cap = A_cap * rmax]
@@ -221,7 +222,9 @@ struct Inst {
   unsigned long long* x_lo;
   double* x_val;
   double* x_pre;
-  int* x_seg;       // segment heads
+  int* x_seg;       // segment heads / entry link ids
+  unsigned long long* y_key;  // entries bucketed by link (stable)
+  double* y_val;
   // ---- Algorithm 1 scratch
   int* g_batches;   // live (undrained) batch list [B_cap]
   int* g_req;       // in-flight unpruned requests [n_req]

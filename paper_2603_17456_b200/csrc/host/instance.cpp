@@ -666,6 +666,7 @@ void carve_instance(Carver& c, const InstanceInput& in, Inst& d, const Inst& top
   const size_t nl = std::max(d.nlinks, 1);
   d.l_res = c.S<double>(nl);
   d.l_cnt = c.S<int>(nl);
+  d.l_off = c.S<int>(nl);
   d.l_x = c.S<double>(nl);
   d.l_y = c.S<double>(nl);
   const size_t pA = static_cast<size_t>(pow2(static_cast<long>(nA)));
@@ -691,6 +692,8 @@ void carve_instance(Carver& c, const InstanceInput& in, Inst& d, const Inst& top
   d.x_val = c.S<double>(pX);
   d.x_pre = c.S<double>(pX);
   d.x_seg = c.S<int>(pX);
+  d.y_key = c.S<unsigned long long>(pX);
+  d.y_val = c.S<double>(pX);
   const size_t pB = static_cast<size_t>(pow2(static_cast<long>(nB)));
   d.g_batches = c.S<int>(nB);
   d.g_req = c.S<int>(nr);
@@ -941,37 +944,30 @@ void Batch::download(int detail) {
 }
 
 void Batch::run(int detail) {
-  upload();
-  launch();
-  download(detail);
-  // capacity retries: double the bound that was hit and rerun just those
-  for (int attempt = 0; attempt < 12; ++attempt) {
-    std::vector<int> redo;
+  // Instances that outgrow a device capacity bound (active set, event pool,
+  // scratch) stop with a capacity check; their bounds are raised and the
+  // whole batch is re-packed and re-run, so the resident layout always holds
+  // the final capacities (a later launch() re-simulates the same batch).
+  for (int attempt = 0; attempt < 16; ++attempt) {
+    upload();
+    launch();
+    download(detail);
+    bool again = false;
     for (int i = 0; i < size(); ++i) {
       const long long chk = outputs_[i].out[OUT_CHECK];
-      if (outputs_[i].out[OUT_STATUS] == ERR_INTERNAL &&
-          (chk == CHK_CAP_ACTIVE || chk == CHK_CAP_SCRATCH || chk == CHK_CAP_EVENTS))
-        redo.push_back(i);
-    }
-    if (redo.empty()) return;
-    std::vector<InstanceInput> again;
-    for (int i : redo) {
-      InstanceInput in = inputs_[i];
-      const long long chk = outputs_[i].out[OUT_CHECK];
-      if (chk == CHK_CAP_EVENTS)
+      if (outputs_[i].out[OUT_STATUS] != ERR_INTERNAL) continue;
+      InstanceInput& in = inputs_[i];
+      if (chk == CHK_CAP_EVENTS) {
         in.e_boost = std::max(in.e_boost * 2, 1024);
-      else
-        in.a_cap = static_cast<int>(std::min<long long>(
-            std::max<long long>(2LL * desc_[i].A_cap, 64), std::max(desc_[i].F_cap, 1)));
-      again.push_back(std::move(in));
+        again = true;
+      } else if (chk == CHK_CAP_ACTIVE || chk == CHK_CAP_SCRATCH) {
+        const long long grown = std::max<long long>(2LL * desc_[i].A_cap, 64);
+        in.a_cap = static_cast<int>(std::min<long long>(grown, std::max(desc_[i].F_cap, 1)));
+        again = true;
+      }
     }
-    Batch sub(be_, std::move(again));
-    sub.run(detail);
-    for (size_t k = 0; k < redo.size(); ++k) {
-      outputs_[redo[k]] = sub.outputs_[k];
-      inputs_[redo[k]].a_cap = sub.inputs_[k].a_cap;
-      inputs_[redo[k]].e_boost = sub.inputs_[k].e_boost;
-    }
+    if (!again) return;
+    pack();
   }
 }
 
