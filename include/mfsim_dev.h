@@ -85,6 +85,10 @@ long long mfsim_dev_d2h_bytes(const mfsim_dev* d);
 long long mfsim_dev_device_bytes(const mfsim_dev* d);
 int mfsim_dev_kernel_launches(const mfsim_dev* d);
 
+/* raw per-instance device counters (events, steps, ..., phase cycles in
+ * profiling builds); returns the number written */
+int mfsim_dev_counters(const mfsim_dev* d, int i, long long* out, int cap);
+
 /* per-request results; done = -1 when unfinished (ttft = done - arrival) */
 int mfsim_dev_requests(const mfsim_dev* d, int i, double* arrival, double* deadline,
                        double* done, unsigned char* pruned, double* stall, int* batch,

@@ -262,6 +262,17 @@ int mfsim_dev_stats_get(const mfsim_dev* d, int i, mfsim_dev_stats* s) {
   });
 }
 
+int mfsim_dev_counters(const mfsim_dev* d, int i, long long* out, int cap) {
+  if (!out) return -1;
+  int n = -1;
+  guarded([&] {
+    const InstanceOutput& o = checked(d, i);
+    n = cap < mfb::OUT_N ? cap : mfb::OUT_N;
+    for (int k = 0; k < n; ++k) out[k] = o.out[k];
+  });
+  return n;
+}
+
 int mfsim_dev_requests(const mfsim_dev* d, int i, double* arrival, double* deadline, double* done,
                        unsigned char* pruned, double* stall, int* batch, long cap) {
   return guarded([&] {

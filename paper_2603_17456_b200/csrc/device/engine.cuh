@@ -88,6 +88,22 @@ MF_FN int popc32(unsigned m) { return __popc(m); }
 MF_FN int ctz32(unsigned m) { return __builtin_ctz(m); }
 MF_FN int popc32(unsigned m) { return __builtin_popcount(m); }
 #endif
+// 1/n correctly rounded for small n (exact table), else a division
+#if defined(__CUDACC__)
+__device__ __constant__ double kRecipTab[65] = {
+#else
+static const double kRecipTab[65] = {
+#endif
+    0.0,     1.0 / 1,  1.0 / 2,  1.0 / 3,  1.0 / 4,  1.0 / 5,  1.0 / 6,  1.0 / 7,  1.0 / 8,
+    1.0 / 9,  1.0 / 10, 1.0 / 11, 1.0 / 12, 1.0 / 13, 1.0 / 14, 1.0 / 15, 1.0 / 16, 1.0 / 17,
+    1.0 / 18, 1.0 / 19, 1.0 / 20, 1.0 / 21, 1.0 / 22, 1.0 / 23, 1.0 / 24, 1.0 / 25, 1.0 / 26,
+    1.0 / 27, 1.0 / 28, 1.0 / 29, 1.0 / 30, 1.0 / 31, 1.0 / 32, 1.0 / 33, 1.0 / 34, 1.0 / 35,
+    1.0 / 36, 1.0 / 37, 1.0 / 38, 1.0 / 39, 1.0 / 40, 1.0 / 41, 1.0 / 42, 1.0 / 43, 1.0 / 44,
+    1.0 / 45, 1.0 / 46, 1.0 / 47, 1.0 / 48, 1.0 / 49, 1.0 / 50, 1.0 / 51, 1.0 / 52, 1.0 / 53,
+    1.0 / 54, 1.0 / 55, 1.0 / 56, 1.0 / 57, 1.0 / 58, 1.0 / 59, 1.0 / 60, 1.0 / 61, 1.0 / 62,
+    1.0 / 63, 1.0 / 64};
+MF_FN double recip(int n) { return n <= 64 ? kRecipTab[n] : ddiv(1.0, (double)n); }
+
 MF_FN int klass_of(int kind) { return kind <= EV_DEPART ? 0 : (kind == EV_TICK ? 2 : 1); }
 MF_FN int pow2ceil(int n) {
   int p = 1;
@@ -113,7 +129,16 @@ struct Sc {
   int err, chk;
   long long pruned;
   int max_active;
+  long long cy[8];
 };
+
+#if defined(MF_PROF) && defined(__CUDACC__)
+#define MF_TIC(v) long long v = clock64()
+#define MF_TOC(slot, v) s.cy[slot - OUT_CY_NEXT] += clock64() - v
+#else
+#define MF_TIC(v)
+#define MF_TOC(slot, v)
+#endif
 
 struct Ev {
   double t;
@@ -242,7 +267,9 @@ struct Engine {
   // ----------------------------------------------------- active flow set
   MF_FN void remove_active(int fid) {  // engine.cpp:251-259
     const int pos = I.f_apos[fid];
-    if (pos < 0) return;
+    if (pos >= 0) remove_active_at(fid, pos);
+  }
+  MF_FN void remove_active_at(int fid, int pos) {
     const int last = s.n_active - 1;
     const int lf = I.a_fid[last];
     g.sync();
@@ -683,6 +710,7 @@ struct Engine {
 
   // promote over a batch (rmlq.cpp:150-193); p2d_only for the periodic tick
   MF_NOINLINE bool promote_batch(int b, bool p2d_only) {
+    MF_TIC(tp);
     const int nx = build_index();
     if (s.err) return false;
     const int lcur = l_curr(b);
@@ -708,6 +736,7 @@ struct Engine {
     }
     g.sync();
     bucket_release(nx);
+    MF_TOC(OUT_CY_PROMOTE, tp);
     s.algo_bytes += 40LL * fc;
     if (g.any(bad)) fail(ERR_INTERNAL, CHK_NEG_MLU);
     if (g.any(urgent_bad)) fail(ERR_INTERNAL, CHK_URGENT_BAND);
@@ -1155,12 +1184,26 @@ struct Engine {
       int nu = n;
       while (nu > 0) {
         ++s.rounds;
-        // inc = min over touched links of max(0, residual) / count and cap gaps
+        // inc = min over touched links of max(0, residual) / count and cap gaps.
+        // The exact quotients are only needed near the minimum: res * (1/cnt)
+        // is within 2 ulp of the correctly rounded res / cnt, so every link
+        // whose exact quotient can be the minimum lies within that margin of
+        // the approximate minimum; only those are divided exactly.
+        double amin = MF_INF;
+        for (int j = g.lane(); j < nt; j += G::N) {
+          const int l = I.s_tl[j];
+          const int cnt = I.l_cnt[l];
+          if (cnt > 0) amin = smin(amin, dmul(smax(0.0, I.l_res[l]), recip(cnt)));
+        }
+        for (int m = G::N / 2; m > 0; m >>= 1) amin = smin(amin, g.shfl_xor(amin, m));
+        const double athr = dadd(amin, dmul(amin, 0x1p-44));
         double inc = MF_INF;
         for (int j = g.lane(); j < nt; j += G::N) {
           const int l = I.s_tl[j];
           const int cnt = I.l_cnt[l];
-          if (cnt > 0) inc = smin(inc, ddiv(smax(0.0, I.l_res[l]), (double)cnt));
+          if (cnt <= 0) continue;
+          const double r = smax(0.0, I.l_res[l]);
+          if (dmul(r, recip(cnt)) <= athr) inc = smin(inc, ddiv(r, (double)cnt));
         }
         if (has_caps) {
           for (int i = g.lane(); i < nu; i += G::N) {
@@ -1235,11 +1278,16 @@ struct Engine {
   // engine.cpp:278-293
   MF_NOINLINE void recompute_rates() {
     bool has_caps = false;
+    MF_TIC(t0);
     int ncls = decide(&has_caps);
+    MF_TOC(OUT_CY_DECIDE, t0);
     if (s.err) return;
     ++s.steps;
+    MF_TIC(t1);
     allocate(ncls, has_caps);
+    MF_TOC(OUT_CY_ALLOC, t1);
     if (s.err) return;
+    MF_TIC(t2);
     const int A = s.n_active;
     unsigned long long seq0 = s.seq;
     int pushed = 0;
@@ -1270,6 +1318,7 @@ struct Engine {
     s.seq += (unsigned long long)pushed;
     s.pushes += pushed;
     s.algo_bytes += 32LL * A;
+    MF_TOC(OUT_CY_RESCHED, t2);
   }
 
   // ===================================================== K1: stage DAG
@@ -1332,50 +1381,60 @@ struct Engine {
   }
 
   MF_NOINLINE void finish_flow(int fid) {  // engine.cpp:318-354
-    if (done(fid)) {
+    // the flow's record in one burst of independent loads
+    const int st = I.f_state[fid];
+    const int pos = I.f_apos[fid];
+    const double size = I.f_size[fid];
+    const int b = I.f_batch[fid];
+    const int c = I.f_cof[fid];
+    const int r = I.f_req[fid];
+    const int stage = I.f_stage[fid];
+    if (st == FL_DONE) {
       fail(ERR_INTERNAL, CHK_FINISHED_TWICE);
       return;
     }
-    const int pos = I.f_apos[fid];
     if (pos >= 0) {
-      double rem = I.a_rem[pos];
-      if (!(rem <= dadd(dmul(1e-6, smax(I.f_size[fid], 1.0)), 1e-9))) {
+      const double rem = I.a_rem[pos];
+      if (!(rem <= dadd(dmul(1e-6, smax(size, 1.0)), 1e-9))) {
         fail(ERR_INTERNAL, CHK_EARLY_FINISH);
         return;
       }
+    }
+    // owners' counters, again in one burst
+    const int bopen = b >= 0 ? I.b_open[b] : 0;
+    const int copen = c >= 0 ? I.c_open[c] : 1;
+    const int ropen = r >= 0 ? I.r_open[r] : 0;
+    const double rlast = r >= 0 ? I.r_lastfin[r] : 0.0;
+    if (!(copen > 0)) {
+      fail(ERR_INTERNAL, CHK_COFLOW_BARRIER);
+      return;
     }
     g.sync();
     if (g.leader()) {
       I.f_state[fid] = FL_DONE;
       I.f_fin[fid] = s.now;
+      if (b >= 0) I.b_open[b] = bopen - 1;
+      if (c >= 0) {
+        I.c_open[c] = copen - 1;
+        if (copen == 1) I.c_done[c] = s.now;
+      }
+      if (r >= 0) {
+        I.r_open[r] = ropen - 1;
+        I.r_lastfin[r] = smax(rlast, s.now);
+      }
     }
     g.sync();
-    remove_active(fid);
+    if (pos >= 0) remove_active_at(fid, pos);
     s.dirty = 1;
-    const int b = I.f_batch[fid];
-    if (b >= 0) put(&I.b_open[b], I.b_open[b] - 1);
-    const int c = I.f_cof[fid];
-    if (c >= 0) {
-      const int open = I.c_open[c];
-      if (!(open > 0)) {
-        fail(ERR_INTERNAL, CHK_COFLOW_BARRIER);
-        return;
-      }
-      put(&I.c_open[c], open - 1);
-      if (open - 1 == 0) {
-        put(&I.c_done[c], s.now);
-        const int cb = I.c_batch[c];
-        on_layer_boundary(cb);
-        if (s.err) return;
-        try_start_layers(cb);
-        check_pipeline_done(cb);
-      }
+    if (c >= 0 && copen == 1) {  // barrier: the pipeline position advances
+      const int cb = I.c_batch[c];
+      on_layer_boundary(cb);
+      if (s.err) return;
+      try_start_layers(cb);
+      check_pipeline_done(cb);
     }
-    const int r = I.f_req[fid];
     if (r >= 0) {
-      put(&I.r_open[r], I.r_open[r] - 1);
-      put(&I.r_lastfin[r], smax(I.r_lastfin[r], s.now));
-      if (I.f_stage[fid] == ST_REUSE && b >= 0) {
+      if (stage == ST_REUSE && b >= 0) {
         try_start_layers(b);
         check_pipeline_done(b);
       }
@@ -1769,7 +1828,9 @@ struct Engine {
   // =============================================== K5: MFS Algorithm 1
   MF_NOINLINE void batch_event_hook() {  // engine.cpp:560-583
     if (I.p.policy != POL_MFS) return;
+    MF_TIC(tb);
     int np = on_batch_event();
+    MF_TOC(OUT_CY_BATCHEV, tb);
     if (s.err || np == 0) return;
     // apply_prunes, ascending request id
     for (int k = 0; k < np; ++k) {
@@ -2178,8 +2239,11 @@ struct Engine {
     }
     recompute_rates();
     s.dirty = 0;
+    for (int k = 0; k < 8; ++k) s.cy[k] = 0;
     while (!s.err) {
+      MF_TIC(tn);
       Ev e = next_event();
+      MF_TOC(OUT_CY_NEXT, tn);
       if (e.src == 0) break;
       if (e.t > s.horizon) break;
       int kind, a, b;
@@ -2198,7 +2262,9 @@ struct Engine {
         a = I.a_fid[e.idx];
         b = -1;
       }
+      MF_TIC(ta);
       advance_to(e.t);
+      MF_TOC(OUT_CY_ADVANCE, ta);
       if (s.err) break;
 #if defined(MF_TRACE) && !defined(__CUDACC__)
       fprintf(stderr, "ev %lld t=%.17g kind=%d a=%d b=%d nact=%d nev=%d\n", s.events, e.t, kind, a, b,
@@ -2214,6 +2280,7 @@ struct Engine {
         s.streak = 0;
         s.prev_t = e.t;
       }
+      MF_TIC(th);
       switch (kind) {
         case EV_FLOW:
           finish_flow(a);
@@ -2249,6 +2316,7 @@ struct Engine {
         default:
           break;
       }
+      MF_TOC(OUT_CY_HANDLER, th);
       if (s.err) break;
       if (s.dirty) {
         recompute_rates();
@@ -2271,6 +2339,7 @@ struct Engine {
       I.out[OUT_NOW_BITS] = (long long)dbits(s.now);
       I.out[OUT_CLASSES] = s.classes;
       I.out[OUT_ROUNDS] = s.rounds;
+      for (int k = 0; k < 8; ++k) I.out[OUT_CY_NEXT + k] = s.cy[k];
     }
     g.sync();
   }

@@ -28,7 +28,7 @@ class EmuBackend final : public Backend {
   void d2h(void* h, const void* d, size_t n) override {
     if (n) std::memcpy(h, d, n);
   }
-  void launch(const mfb::Inst* d, int n, const LaunchHint&) override {
+  void launch(const mfb::Inst* d, const int*, int n, const LaunchHint&) override {
     for (int i = 0; i < n; ++i) {
       mfb::Inst local = d[i];
       mfb::Engine<mfb::SerialLanes> eng(local);

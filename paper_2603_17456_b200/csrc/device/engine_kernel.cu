@@ -45,8 +45,8 @@ __host__ inline SmemPlan make_plan(int rmax, int nlinks) {
 }
 
 __global__ void __launch_bounds__(32)
-    mfsim_engine_kernel(const Inst* __restrict__ insts, int n, int* __restrict__ next,
-                        SmemPlan plan) {
+    mfsim_engine_kernel(const Inst* __restrict__ insts, const int* __restrict__ order, int n,
+                        int* __restrict__ next, SmemPlan plan) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31;
   Inst* d = reinterpret_cast<Inst*>(smem);
@@ -55,6 +55,7 @@ __global__ void __launch_bounds__(32)
     if (lane == 0) i = atomicAdd(next, 1);
     i = __shfl_sync(0xffffffffu, i, 0);
     if (i >= n) return;
+    i = order[i];  // longest estimated instances first
     // descriptor copy (8-byte words across the warp)
     {
       const unsigned long long* src = reinterpret_cast<const unsigned long long*>(insts + i);
@@ -168,7 +169,7 @@ class CudaBackend final : public Backend {
   void d2h(void* h, const void* d, size_t n) override {
     if (n) ck(cudaMemcpyAsync(h, d, n, cudaMemcpyDeviceToHost, stream_), "D2H");
   }
-  void launch(const mfb::Inst* d, int n, const LaunchHint& hint) override {
+  void launch(const mfb::Inst* d, const int* order, int n, const LaunchHint& hint) override {
     const mfb::SmemPlan plan = mfb::make_plan(hint.rmax, hint.nlinks);
     int per_sm = 0;
     ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mfb::mfsim_engine_kernel, 32,
@@ -179,7 +180,7 @@ class CudaBackend final : public Backend {
     if (n < grid) grid = n > 0 ? n : 1;
     ck(cudaMemsetAsync(counter_, 0, sizeof(int), stream_), "memset");
     ck(cudaEventRecord(e0_, stream_), "event");
-    mfb::mfsim_engine_kernel<<<grid, 32, plan.bytes, stream_>>>(d, n, counter_, plan);
+    mfb::mfsim_engine_kernel<<<grid, 32, plan.bytes, stream_>>>(d, order, n, counter_, plan);
     ck(cudaGetLastError(), "launch");
     ck(cudaEventRecord(e1_, stream_), "event");
     ++launches_;

@@ -273,7 +273,16 @@ enum : int {
   OUT_NOW_BITS,
   OUT_CLASSES,
   OUT_ROUNDS,
-  OUT_N = 16
+  // phase cycle counters (profiling builds, -DMF_PROF)
+  OUT_CY_NEXT = 16,
+  OUT_CY_ADVANCE,
+  OUT_CY_HANDLER,
+  OUT_CY_DECIDE,
+  OUT_CY_ALLOC,
+  OUT_CY_RESCHED,
+  OUT_CY_BATCHEV,
+  OUT_CY_PROMOTE,
+  OUT_N = 24
 };
 
 }  // namespace mfb

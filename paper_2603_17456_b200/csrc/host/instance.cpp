@@ -824,8 +824,10 @@ void Batch::release() {
   if (st_dev_) be_.dev_free(st_dev_);
   if (out_dev_) be_.dev_free(out_dev_);
   if (desc_dev_) be_.dev_free(desc_dev_);
+  if (order_dev_) be_.dev_free(order_dev_);
   in_host_ = out_host_ = in_dev_ = st_dev_ = out_dev_ = nullptr;
   desc_dev_ = nullptr;
+  order_dev_ = nullptr;
 }
 
 void Batch::pack() {
@@ -872,16 +874,30 @@ void Batch::pack() {
       st_dev_ = static_cast<char*>(be_.dev_alloc(st_bytes_ + 64));
       out_dev_ = static_cast<char*>(be_.dev_alloc(out_bytes_ + 64));
       desc_dev_ = static_cast<Inst*>(be_.dev_alloc(sizeof(Inst) * std::max(n, 1)));
+      order_dev_ = static_cast<int*>(be_.dev_alloc(sizeof(int) * std::max(n, 1)));
     }
   }
+  // claim order: estimated work descending (Karuna's capped filling and MFS's
+  // promotions cost the most per event), so the longest instances start first
+  std::vector<double> cost(n);
+  for (int i = 0; i < n; ++i) {
+    const Inst& d = desc_[i];
+    static const double factor[] = {1.0, 1.6, 1.1, 12.0, 2.5};
+    const int pol = d.p.policy >= 0 && d.p.policy < 5 ? d.p.policy : 0;
+    cost[i] = factor[pol] * (double(d.F_cap) + 2.0 * d.n_req);
+  }
+  order_.resize(n);
+  std::iota(order_.begin(), order_.end(), 0);
+  std::stable_sort(order_.begin(), order_.end(), [&](int a, int b) { return cost[a] > cost[b]; });
 }
 
 void Batch::upload() {
   be_.h2d(in_dev_, in_host_, in_bytes_);
   be_.h2d(desc_dev_, desc_.data(), sizeof(Inst) * desc_.size());
+  be_.h2d(order_dev_, order_.data(), sizeof(int) * order_.size());
 }
 
-void Batch::launch() { be_.launch(desc_dev_, size(), hint_); }
+void Batch::launch() { be_.launch(desc_dev_, order_dev_, size(), hint_); }
 
 size_t Batch::output_bytes(int detail) const {
   size_t b = out_bytes_;

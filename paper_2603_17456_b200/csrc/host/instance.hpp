@@ -43,7 +43,8 @@ class Backend {
   virtual void host_free(void* p) = 0;
   virtual void h2d(void* dst, const void* src, size_t n) = 0;  // stream-ordered
   virtual void d2h(void* dst, const void* src, size_t n) = 0;
-  virtual void launch(const mfb::Inst* d_insts, int n, const LaunchHint& hint) = 0;
+  // order: device array, a permutation of [0, n) giving the claim order
+  virtual void launch(const mfb::Inst* d_insts, const int* order, int n, const LaunchHint& hint) = 0;
   virtual void sync() = 0;
   virtual void set_stream(void* stream) = 0;
   virtual double last_kernel_ms() const = 0;
@@ -139,6 +140,8 @@ class Batch {
   char* st_dev_ = nullptr;
   char* out_dev_ = nullptr;
   mfb::Inst* desc_dev_ = nullptr;
+  int* order_dev_ = nullptr;
+  std::vector<int> order_;
   LaunchHint hint_;
   size_t in_bytes_ = 0, st_bytes_ = 0, out_bytes_ = 0;
   struct OutView {

@@ -111,6 +111,7 @@ class Native:
             "mfsim_dev_requests_csv": ([vp, i, C.POINTER(C.c_void_p)], i),
             "mfsim_dev_write_report": ([vp, i, cp], i),
             "mfsim_route": ([vp, i, i, vp, vp, i, C.POINTER(i)], i),
+            "mfsim_dev_counters": ([vp, i, vp, i], i),
             "mfsim_link_count": ([vp, C.POINTER(i)], i),
         }
         for name, (args, res) in sig.items():
@@ -280,6 +281,11 @@ class DeviceBatch:
             self.n.check(self.n.lib.mfsim_dev_requests_csv(self.h, i, C.byref(p)))
             r.requests_csv = self.n.take_string(p)
         return r
+
+    def counters(self, i: int) -> np.ndarray:
+        out = np.zeros(32, np.int64)
+        n = self.n.lib.mfsim_dev_counters(self.h, i, _ptr(out), 32)
+        return out[:max(n, 0)]
 
     def raise_for_status(self, i: int):
         st = self.stats(i)
