@@ -215,38 +215,62 @@ struct Engine {
     ++s.pushes;
   }
 
+  // K4: the earliest of the arrival head, the event pool and the per-flow
+  // completion slots under (t, klass, seq) (engine.hpp:182-188). klass and seq
+  // share one 64-bit key (seq < 2^61); source and index share one int.
   MF_FN Ev next_event() {
-    Ev best;
-    best.t = MF_INF;
-    best.klass = 3;
-    best.seq = kNoSeq;
-    best.src = 0;
-    best.idx = -1;
+    const int ne = s.n_ev, na = s.n_active;
+    const double* __restrict__ et = I.e_t;
+    const unsigned long long* __restrict__ es = I.e_seq;
+    const int* __restrict__ ek = I.e_kind;
+    const double* __restrict__ at = I.a_evt;
+    const unsigned long long* __restrict__ as = I.a_evseq;
+    double bt = MF_INF;
+    unsigned long long bk = ~0ull;
+    int bsi = 0;  // (src << 28) | idx, src 0 = none
     if (g.leader() && s.next_arr < I.n_arr) {
-      int r = I.arr_order[s.next_arr];
-      Ev c{I.r_arrival[r], 1, (unsigned long long)r, 1, r};
-      best = c;
+      const int r = I.arr_order[s.next_arr];
+      bt = I.r_arrival[r];
+      bk = (1ull << 61) | (unsigned long long)r;
+      bsi = (1 << 28) | r;
     }
-    for (int i = g.lane(); i < s.n_ev; i += G::N) {
-      Ev c{I.e_t[i], klass_of(I.e_kind[i]), I.e_seq[i], 2, i};
-      if (best.src == 0 || ev_less(c, best)) best = c;
+#pragma unroll 2
+    for (int i = g.lane(); i < ne; i += G::N) {
+      const double t = et[i];
+      const unsigned long long k = ((unsigned long long)klass_of(ek[i]) << 61) | es[i];
+      if (t < bt || (t == bt && k < bk)) {
+        bt = t;
+        bk = k;
+        bsi = (2 << 28) | i;
+      }
     }
-    for (int p = g.lane(); p < s.n_active; p += G::N) {
-      unsigned long long q = I.a_evseq[p];
-      if (q == kNoSeq) continue;
-      Ev c{I.a_evt[p], 0, q, 3, p};
-      if (best.src == 0 || ev_less(c, best)) best = c;
+#pragma unroll 4
+    for (int p = g.lane(); p < na; p += G::N) {
+      const unsigned long long k = as[p];
+      const double t = at[p];
+      if (k != kNoSeq && (t < bt || (t == bt && k < bk))) {
+        bt = t;
+        bk = k;
+        bsi = (3 << 28) | p;
+      }
     }
     for (int m = G::N / 2; m > 0; m >>= 1) {
-      Ev o;
-      o.t = g.shfl_xor(best.t, m);
-      o.klass = g.shfl_xor(best.klass, m);
-      o.seq = g.shfl_xor(best.seq, m);
-      o.src = g.shfl_xor(best.src, m);
-      o.idx = g.shfl_xor(best.idx, m);
-      if (o.src != 0 && (best.src == 0 || ev_less(o, best))) best = o;
+      const double ot = g.shfl_xor(bt, m);
+      const unsigned long long ok = g.shfl_xor(bk, m);
+      const int os = g.shfl_xor(bsi, m);
+      if (ot < bt || (ot == bt && ok < bk)) {
+        bt = ot;
+        bk = ok;
+        bsi = os;
+      }
     }
-    s.algo_bytes += 16LL * s.n_active + 24LL * s.n_ev;
+    Ev best;
+    best.t = bt;
+    best.klass = (int)(bk >> 61);
+    best.seq = bk & ((1ull << 61) - 1);
+    best.src = bsi >> 28;
+    best.idx = bsi & ((1 << 28) - 1);
+    s.algo_bytes += 16LL * na + 24LL * ne;
     return best;
   }
 
@@ -296,18 +320,22 @@ struct Engine {
       return;
     }
     if (dt > 0.0) {
+      const int na = s.n_active;
+      double* __restrict__ rem = I.a_rem;
+      const double* __restrict__ rt = I.a_rate;
       bool bad = false;
-      for (int p = g.lane(); p < s.n_active; p += G::N) {
-        double rem = dsub(I.a_rem[p], dmul(I.a_rate[p], dt));
-        if (rem < 0.0) {
-          double sz = I.f_size[I.a_fid[p]];
-          if (!(rem > dsub(-dmul(1e-6, smax(sz, 1.0)), 1e-9))) bad = true;
-          rem = 0.0;
+#pragma unroll 4
+      for (int p = g.lane(); p < na; p += G::N) {
+        double x = dsub(rem[p], dmul(rt[p], dt));
+        if (x < 0.0) {
+          const double sz = I.f_size[I.a_fid[p]];
+          if (!(x > dsub(-dmul(1e-6, smax(sz, 1.0)), 1e-9))) bad = true;
+          x = 0.0;
         }
-        I.a_rem[p] = rem;
+        rem[p] = x;
       }
       g.sync();
-      s.algo_bytes += 24LL * s.n_active;
+      s.algo_bytes += 24LL * na;
       if (g.any(bad)) {
         fail(ERR_INTERNAL, CHK_OVERSHOOT);
         return;
@@ -1120,108 +1148,132 @@ struct Engine {
   MF_NOINLINE void allocate(int ncls, bool has_caps) {
     const int A = s.n_active;
     const int RM = I.rmax;
+    int* __restrict__ ord = I.s_ord;
+    const int* __restrict__ afid = I.a_fid;
+    const unsigned short* __restrict__ arlp = I.a_rl;
+    const uint8_t* __restrict__ arnp = I.a_rn;
+    double* __restrict__ res = I.l_res;
+    int* __restrict__ cnt = I.l_cnt;
+    double* __restrict__ rate = I.s_rate;
+    int* __restrict__ ul = I.s_ul;
+    unsigned short* __restrict__ tl = I.s_tl;
+    const double* __restrict__ capv = I.cap;
+    const double* __restrict__ scap = I.s_cap;
     // rate-map insertion order for the load_fraction hash emulation
-    for (int i = g.lane(); i < A; i += G::N) {
-      int fid = I.a_fid[I.s_ord[i]];
-      I.h_keys[i] = fid;
-      I.f_hidx[fid] = i;
+    {
+      int* __restrict__ hk = I.h_keys;
+      int* __restrict__ hidx = I.f_hidx;
+      for (int i = g.lane(); i < A; i += G::N) {
+        const int fid = afid[ord[i]];
+        hk[i] = fid;
+        hidx[fid] = i;
+      }
     }
     g.sync();
     s.h_n = A;
     s.h_ready = 0;
+    long long rounds = 0, bytes = 0;
     for (int c = 0; c < ncls; ++c) {
       const int o0 = I.s_cls[c], o1 = I.s_cls[c + 1];
       const int n = o1 - o0;
-      ++s.classes;
       if (n == 1) {  // singleton: bottleneck residual, capped (allocator.cpp:42-59)
-        const int p = I.s_ord[o0];
-        const int rn = arn(p);
+        const int p = ord[o0];
+        const int rn = arnp[p];
         double r = MF_INF;
         if (has_caps) {
-          double cp = I.s_cap[p];
+          const double cp = scap[p];
           if (cp < MF_INF) r = smax(0.0, cp);
         }
-        // lanes gather the route's residuals; min in route order is order-free
         double mine = MF_INF;
-        if (g.lane() < rn) mine = smax(0.0, I.l_res[arl(p, g.lane())]);
-        for (int k = G::N; k < rn; ++k) mine = smin(mine, smax(0.0, I.l_res[arl(p, k)]));
+        for (int k = g.lane(); k < rn; k += G::N) mine = smin(mine, smax(0.0, res[arlp[p * RM + k]]));
         for (int m = G::N / 2; m > 0; m >>= 1) mine = smin(mine, g.shfl_xor(mine, m));
         r = smin(r, mine);
         g.sync();
         for (int k = g.lane(); k < rn; k += G::N) {
-          const int l = arl(p, k);
-          I.l_res[l] = dsub(I.l_res[l], r);
+          const int l = arlp[p * RM + k];
+          res[l] = dsub(res[l], r);
         }
-        if (g.leader()) I.s_rate[p] = r;
+        if (g.leader()) rate[p] = r;
         g.sync();
-        s.algo_bytes += 20LL * rn + 12;
+        bytes += 20LL * rn + 12;
         continue;
       }
       // multi-flow class: members start unfrozen at rate 0; count per link
       int nt = 0;
       for (int base = 0; base < n; base += G::N) {
         const int i = base + g.lane();
-        int p = -1, rn = 0;
+        int p = 0, rn = 0;
         if (i < n) {
-          p = I.s_ord[o0 + i];
-          rn = arn(p);
-          I.s_rate[p] = 0.0;
-          I.s_ul[i] = p;
+          p = ord[o0 + i];
+          rn = arnp[p];
+          rate[p] = 0.0;
+          ul[i] = p;
         }
         for (int k = 0; k < RM; ++k) {
           bool first = false;
           int l = 0;
           if (k < rn) {
-            l = arl(p, k);
-            first = g.atomic_add(&I.l_cnt[l], 1) == 0;
+            l = arlp[p * RM + k];
+            first = g.atomic_add(&cnt[l], 1) == 0;
           }
           const unsigned m = g.ballot(first);
-          if (first) I.s_tl[nt + popc32(m & ((1u << g.lane()) - 1u))] = (unsigned short)l;
+          if (first) tl[nt + popc32(m & g.lanemask_lt())] = (unsigned short)l;
           nt += popc32(m);
         }
       }
       g.sync();
       int nu = n;
       while (nu > 0) {
-        ++s.rounds;
+        ++rounds;
         // inc = min over touched links of max(0, residual) / count and cap gaps.
         // The exact quotients are only needed near the minimum: res * (1/cnt)
         // is within 2 ulp of the correctly rounded res / cnt, so every link
         // whose exact quotient can be the minimum lies within that margin of
         // the approximate minimum; only those are divided exactly.
         double amin = MF_INF;
+#pragma unroll 4
         for (int j = g.lane(); j < nt; j += G::N) {
-          const int l = I.s_tl[j];
-          const int cnt = I.l_cnt[l];
-          if (cnt > 0) amin = smin(amin, dmul(smax(0.0, I.l_res[l]), recip(cnt)));
+          const int l = tl[j];
+          const int cn = cnt[l];
+          const double r = res[l];
+          if (cn > 0) amin = smin(amin, dmul(smax(0.0, r), recip(cn)));
         }
-        for (int m = G::N / 2; m > 0; m >>= 1) amin = smin(amin, g.shfl_xor(amin, m));
-        const double athr = dadd(amin, dmul(amin, 0x1p-44));
-        double inc = MF_INF;
-        for (int j = g.lane(); j < nt; j += G::N) {
-          const int l = I.s_tl[j];
-          const int cnt = I.l_cnt[l];
-          if (cnt <= 0) continue;
-          const double r = smax(0.0, I.l_res[l]);
-          if (dmul(r, recip(cnt)) <= athr) inc = smin(inc, ddiv(r, (double)cnt));
-        }
+        double cmin = MF_INF;
         if (has_caps) {
+#pragma unroll 4
           for (int i = g.lane(); i < nu; i += G::N) {
-            const int p = I.s_ul[i];
-            const double cp = I.s_cap[p];
-            if (cp < MF_INF) inc = smin(inc, dsub(smax(0.0, cp), I.s_rate[p]));
+            const int p = ul[i];
+            const double cp = scap[p];
+            if (cp < MF_INF) cmin = smin(cmin, dsub(smax(0.0, cp), rate[p]));
           }
         }
-        for (int m = G::N / 2; m > 0; m >>= 1) inc = smin(inc, g.shfl_xor(inc, m));
-        inc = smax(inc, 0.0);
-        for (int i = g.lane(); i < nu; i += G::N) {
-          const int p = I.s_ul[i];
-          I.s_rate[p] = dadd(I.s_rate[p], inc);
+        for (int m = G::N / 2; m > 0; m >>= 1) {
+          amin = smin(amin, g.shfl_xor(amin, m));
+          cmin = smin(cmin, g.shfl_xor(cmin, m));
         }
+        const double athr = dadd(amin, dmul(amin, 0x1p-44));
+        double inc = cmin;
+        if (amin <= cmin) {  // a link share may be the minimum: exact quotients near it
+#pragma unroll 4
+          for (int j = g.lane(); j < nt; j += G::N) {
+            const int l = tl[j];
+            const int cn = cnt[l];
+            const double r = smax(0.0, res[l]);
+            if (cn > 0 && dmul(r, recip(cn)) <= athr) inc = smin(inc, ddiv(r, (double)cn));
+          }
+          for (int m = G::N / 2; m > 0; m >>= 1) inc = smin(inc, g.shfl_xor(inc, m));
+        }
+        inc = smax(inc, 0.0);
+#pragma unroll 4
+        for (int i = g.lane(); i < nu; i += G::N) {
+          const int p = ul[i];
+          rate[p] = dadd(rate[p], inc);
+        }
+#pragma unroll 4
         for (int j = g.lane(); j < nt; j += G::N) {
-          const int l = I.s_tl[j];
-          const int cnt = I.l_cnt[l];
-          if (cnt > 0) I.l_res[l] = dsub(I.l_res[l], dmul(inc, (double)cnt));
+          const int l = tl[j];
+          const int cn = cnt[l];
+          if (cn > 0) res[l] = dsub(res[l], dmul(inc, (double)cn));
         }
         g.sync();
         // freeze at the cap or on a saturated link; compact the unfrozen list
@@ -1230,33 +1282,33 @@ struct Engine {
         for (int base = 0; base < nu; base += G::N) {
           const int i = base + g.lane();
           bool keep = false;
-          int p = -1;
+          int p = 0;
           if (i < nu) {
-            p = I.s_ul[i];
+            p = ul[i];
             double cp = MF_INF;
             if (has_caps) {
-              const double c0 = I.s_cap[p];
+              const double c0 = scap[p];
               if (c0 < MF_INF) cp = smax(0.0, c0);
             }
             const double cap_eps = dmul(1e-12, smax(1.0, cp == MF_INF ? 0.0 : cp));
-            bool stop = I.s_rate[p] >= dsub(cp, cap_eps);
-            const int rn = arn(p);
-            for (int k = 0; k < rn && !stop; ++k) {
-              const int l = arl(p, k);
-              if (I.l_res[l] <= dmul(1e-12, I.cap[l])) stop = true;
+            bool stop = rate[p] >= dsub(cp, cap_eps);
+            const int rn = arnp[p];
+            for (int k = 0; k < rn; ++k) {
+              const int l = arlp[p * RM + k];
+              if (res[l] <= dmul(1e-12, capv[l])) stop = true;
             }
             keep = !stop;
             if (stop)  // a frozen member leaves every link count for good
-              for (int k = 0; k < rn; ++k) g.atomic_add(&I.l_cnt[arl(p, k)], -1);
+              for (int k = 0; k < rn; ++k) g.atomic_add(&cnt[arlp[p * RM + k]], -1);
           }
           g.sync();  // every lane has read its entry before the in-place compaction
           const unsigned m = g.ballot(keep);
-          if (keep) I.s_ul[keep_n + popc32(m & ((1u << g.lane()) - 1u))] = p;
+          if (keep) ul[keep_n + popc32(m & g.lanemask_lt())] = p;
           keep_n += popc32(m);
           if (i < nu && !keep) froze = true;
         }
         g.sync();
-        s.algo_bytes += (long long)nu * (20LL * RM + 29) + 32LL * nt;
+        bytes += (long long)nu * (20LL * RM + 29) + 32LL * nt;
         if (!g.any(froze)) {
           fail(ERR_INTERNAL, CHK_NO_PROGRESS);
           return;
@@ -1266,13 +1318,16 @@ struct Engine {
     }
     // restore l_res == capacity on every link a route of this step touched
     for (int p = g.lane(); p < A; p += G::N) {
-      const int rn = arn(p);
+      const int rn = arnp[p];
       for (int k = 0; k < rn; ++k) {
-        const int l = arl(p, k);
-        I.l_res[l] = I.cap[l];
+        const int l = arlp[p * RM + k];
+        res[l] = capv[l];
       }
     }
     g.sync();
+    s.classes += ncls;
+    s.rounds += rounds;
+    s.algo_bytes += bytes;
   }
 
   // engine.cpp:278-293
@@ -1289,30 +1344,35 @@ struct Engine {
     if (s.err) return;
     MF_TIC(t2);
     const int A = s.n_active;
-    unsigned long long seq0 = s.seq;
+    const unsigned long long seq0 = s.seq;
+    const double now = s.now;
+    const double* __restrict__ nr = I.s_rate;
+    double* __restrict__ rt = I.a_rate;
+    const double* __restrict__ rem = I.a_rem;
+    double* __restrict__ evt = I.a_evt;
+    unsigned long long* __restrict__ evs = I.a_evseq;
     int pushed = 0;
     for (int base = 0; base < A; base += G::N) {
-      int p = base + g.lane();
+      const int p = base + g.lane();
       int c = 0;
       double r = 0.0;
       bool chg = false;
       if (p < A) {
-        r = I.s_rate[p];
-        chg = !(r == I.a_rate[p]);
+        r = nr[p];
+        chg = !(r == rt[p]);  // exact: unchanged rates keep their old event
         c = (chg && r > 0.0) ? 1 : 0;
       }
-      int tot;
-      int off = g.excl_scan(c, &tot);
+      const unsigned m = g.ballot(c != 0);
       if (chg) {
-        I.a_rate[p] = r;
+        rt[p] = r;
         if (r > 0.0) {
-          I.a_evt[p] = dadd(s.now, ddiv(I.a_rem[p], r));
-          I.a_evseq[p] = seq0 + (unsigned long long)(pushed + off);
+          evt[p] = dadd(now, ddiv(rem[p], r));
+          evs[p] = seq0 + (unsigned long long)(pushed + popc32(m & g.lanemask_lt()));
         } else {
-          I.a_evseq[p] = kNoSeq;
+          evs[p] = kNoSeq;
         }
       }
-      pushed += tot;
+      pushed += popc32(m);
     }
     g.sync();
     s.seq += (unsigned long long)pushed;
