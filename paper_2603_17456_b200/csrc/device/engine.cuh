@@ -75,6 +75,15 @@ MF_FN unsigned long long dbits(double x) {
 }
 MF_FN bool isnan_(double x) { return x != x; }
 #endif
+#if defined(__CUDACC__)
+MF_FN double bits_to_d(unsigned long long u) { return __longlong_as_double((long long)u); }
+#else
+MF_FN double bits_to_d(unsigned long long u) {
+  double d;
+  memcpy(&d, &u, 8);
+  return d;
+}
+#endif
 // order-preserving map double -> u64 (non-NaN; -0 folded onto +0)
 MF_FN unsigned long long dord(double x) {
   if (x == 0.0) x = 0.0;
@@ -88,6 +97,14 @@ MF_FN int popc32(unsigned m) { return __popc(m); }
 MF_FN int ctz32(unsigned m) { return __builtin_ctz(m); }
 MF_FN int popc32(unsigned m) { return __builtin_popcount(m); }
 #endif
+// Tell the compiler a pointer addresses shared memory (LDS/STS/ATOMS instead
+// of generic accesses) when the instance's hot arrays were staged on chip.
+#if defined(__CUDACC__)
+#define MF_SH(ptr) __builtin_assume(__isShared(ptr))
+#else
+#define MF_SH(ptr) ((void)0)
+#endif
+
 // 1/n correctly rounded for small n (exact table), else a division
 #if defined(__CUDACC__)
 __device__ __constant__ double kRecipTab[65] = {
@@ -103,6 +120,11 @@ static const double kRecipTab[65] = {
     1.0 / 54, 1.0 / 55, 1.0 / 56, 1.0 / 57, 1.0 / 58, 1.0 / 59, 1.0 / 60, 1.0 / 61, 1.0 / 62,
     1.0 / 63, 1.0 / 64};
 MF_FN double recip(int n) { return n <= 64 ? kRecipTab[n] : ddiv(1.0, (double)n); }
+#if defined(__CUDACC__)
+MF_FN double frecip(int n) { return (double)__frcp_rn((float)n); }
+#else
+MF_FN double frecip(int n) { return (double)(1.0f / (float)n); }
+#endif
 
 MF_FN int klass_of(int kind) { return kind <= EV_DEPART ? 0 : (kind == EV_TICK ? 2 : 1); }
 MF_FN int pow2ceil(int n) {
@@ -129,7 +151,7 @@ struct Sc {
   int err, chk;
   long long pruned;
   int max_active;
-  long long cy[8];
+  long long cy[32];
 };
 
 #if defined(MF_PROF) && defined(__CUDACC__)
@@ -154,7 +176,9 @@ MF_FN bool ev_less(const Ev& x, const Ev& y) {
   return x.seq < y.seq;
 }
 
-template <class G>
+// kOnChip: active-flow arrays staged in shared memory; kLinksOnChip: per-link
+// residual / count arrays staged too (the common case; see engine_kernel.cu).
+template <class G, bool kOnChip = false, bool kLinksOnChip = false>
 struct Engine {
   G g;
   Inst& I;  // per-warp copy (shared memory on the device), arrays possibly re-pointed
@@ -225,6 +249,10 @@ struct Engine {
     const int* __restrict__ ek = I.e_kind;
     const double* __restrict__ at = I.a_evt;
     const unsigned long long* __restrict__ as = I.a_evseq;
+    if (kOnChip) {
+      MF_SH(at);
+      MF_SH(as);
+    }
     double bt = MF_INF;
     unsigned long long bk = ~0ull;
     int bsi = 0;  // (src << 28) | idx, src 0 = none
@@ -323,6 +351,10 @@ struct Engine {
       const int na = s.n_active;
       double* __restrict__ rem = I.a_rem;
       const double* __restrict__ rt = I.a_rate;
+      if (kOnChip) {
+        MF_SH(rem);
+        MF_SH(rt);
+      }
       bool bad = false;
 #pragma unroll 4
       for (int p = g.lane(); p < na; p += G::N) {
@@ -1159,6 +1191,7 @@ struct Engine {
     unsigned short* __restrict__ tl = I.s_tl;
     const double* __restrict__ capv = I.cap;
     const double* __restrict__ scap = I.s_cap;
+    MF_TIC(q0);
     // rate-map insertion order for the load_fraction hash emulation
     {
       int* __restrict__ hk = I.h_keys;
@@ -1170,6 +1203,7 @@ struct Engine {
       }
     }
     g.sync();
+    MF_TOC(OUT_CY_SUB + 0, q0);
     s.h_n = A;
     s.h_ready = 0;
     long long rounds = 0, bytes = 0;
@@ -1198,16 +1232,26 @@ struct Engine {
         bytes += 20LL * rn + 12;
         continue;
       }
-      // multi-flow class: members start unfrozen at rate 0; count per link
+      // multi-flow class (allocator.cpp:61-121). Every unfrozen member has
+      // received the same sequence of increments from 0, so they share one
+      // rate R; a member's rate is R at the round it freezes. Per round:
+      //   inc = max(min(min_l max(0,res_l)/cnt_l, capmin - R), 0)
+      //   R += inc; res_l -= inc * cnt_l on links with unfrozen members
+      //   freeze members with R >= cap - eps (a prefix of the cap order,
+      //   since cap - 1e-12*max(1,cap) is increasing in cap) and members of
+      //   links whose residual fell to <= 1e-12 * capacity.
+      MF_TIC(q1);
       int nt = 0;
+      int ncap = 0;
       for (int base = 0; base < n; base += G::N) {
         const int i = base + g.lane();
         int p = 0, rn = 0;
+        bool capped = false;
         if (i < n) {
           p = ord[o0 + i];
           rn = arnp[p];
-          rate[p] = 0.0;
-          ul[i] = p;
+          I.s_frz[p] = 0;
+          if (has_caps) capped = scap[p] < MF_INF;
         }
         for (int k = 0; k < RM; ++k) {
           bool first = false;
@@ -1220,103 +1264,137 @@ struct Engine {
           if (first) tl[nt + popc32(m & g.lanemask_lt())] = (unsigned short)l;
           nt += popc32(m);
         }
+        const unsigned mc = g.ballot(capped);
+        if (capped) {  // (cap, position) for the cap order
+          const int slot = ncap + popc32(mc & g.lanemask_lt());
+          I.x_hi[slot] = dbits(smax(0.0, scap[p]));
+          I.x_lo[slot] = (unsigned long long)p;
+        }
+        ncap += popc32(mc);
       }
       g.sync();
+      // link -> member incidence: offsets from the counts, then fill
+      int* __restrict__ loff = I.l_off;
+      int* __restrict__ mem = I.s_mem;
+      {
+        int off = 0;
+        for (int base = 0; base < nt; base += G::N) {
+          const int j = base + g.lane();
+          int c0 = 0, l = 0;
+          if (j < nt) {
+            l = tl[j];
+            c0 = cnt[l];
+          }
+          int tot;
+          const int o = g.excl_scan(c0, &tot);
+          if (j < nt) {
+            loff[l] = off + o;
+            I.l_mb[l] = off + o;
+          }
+          off += tot;
+        }
+        g.sync();
+        for (int i = g.lane(); i < n; i += G::N) {
+          const int p = ord[o0 + i];
+          const int rn = arnp[p];
+          for (int k = 0; k < rn; ++k) {
+            const int l = arlp[p * RM + k];
+            mem[g.atomic_add(&loff[l], 1)] = p;
+          }
+        }
+        g.sync();  // l's members: [l_mb[l], loff[l])
+      }
+      if (ncap > 1) sort_x(ncap);  // caps ascending (cap >= 0: bit order)
+      MF_TOC(OUT_CY_SUB + 1, q1);
       int nu = n;
+      int cptr = 0;
+      double R = 0.0;
       while (nu > 0) {
         ++rounds;
-        // inc = min over touched links of max(0, residual) / count and cap gaps.
-        // The exact quotients are only needed near the minimum: res * (1/cnt)
-        // is within 2 ulp of the correctly rounded res / cnt, so every link
-        // whose exact quotient can be the minimum lies within that margin of
-        // the approximate minimum; only those are divided exactly.
+        MF_TIC(q2);
+        // capmin over unfrozen capped members (frozen ones skipped lazily)
+        while (cptr < ncap && I.s_frz[(int)I.x_lo[cptr]]) ++cptr;
+        const double cmin = cptr < ncap ? dsub(bits_to_d(I.x_hi[cptr]), R) : MF_INF;
         double amin = MF_INF;
 #pragma unroll 4
         for (int j = g.lane(); j < nt; j += G::N) {
           const int l = tl[j];
           const int cn = cnt[l];
           const double r = res[l];
-          if (cn > 0) amin = smin(amin, dmul(smax(0.0, r), recip(cn)));
+          if (cn > 0) amin = smin(amin, dmul(smax(0.0, r), frecip(cn)));
         }
-        double cmin = MF_INF;
-        if (has_caps) {
-#pragma unroll 4
-          for (int i = g.lane(); i < nu; i += G::N) {
-            const int p = ul[i];
-            const double cp = scap[p];
-            if (cp < MF_INF) cmin = smin(cmin, dsub(smax(0.0, cp), rate[p]));
-          }
-        }
-        for (int m = G::N / 2; m > 0; m >>= 1) {
-          amin = smin(amin, g.shfl_xor(amin, m));
-          cmin = smin(cmin, g.shfl_xor(cmin, m));
-        }
-        const double athr = dadd(amin, dmul(amin, 0x1p-44));
+        for (int m = G::N / 2; m > 0; m >>= 1) amin = smin(amin, g.shfl_xor(amin, m));
         double inc = cmin;
-        if (amin <= cmin) {  // a link share may be the minimum: exact quotients near it
+        if (amin <= cmin) {  // exact quotients only within the approximation margin
+          const double athr = dadd(amin, dmul(amin, 0x1p-18));
 #pragma unroll 4
           for (int j = g.lane(); j < nt; j += G::N) {
             const int l = tl[j];
             const int cn = cnt[l];
             const double r = smax(0.0, res[l]);
-            if (cn > 0 && dmul(r, recip(cn)) <= athr) inc = smin(inc, ddiv(r, (double)cn));
+            if (cn > 0 && dmul(r, frecip(cn)) <= athr) inc = smin(inc, ddiv(r, (double)cn));
           }
           for (int m = G::N / 2; m > 0; m >>= 1) inc = smin(inc, g.shfl_xor(inc, m));
         }
         inc = smax(inc, 0.0);
-#pragma unroll 4
-        for (int i = g.lane(); i < nu; i += G::N) {
-          const int p = ul[i];
-          rate[p] = dadd(rate[p], inc);
-        }
-#pragma unroll 4
-        for (int j = g.lane(); j < nt; j += G::N) {
-          const int l = tl[j];
-          const int cn = cnt[l];
-          if (cn > 0) res[l] = dsub(res[l], dmul(inc, (double)cn));
-        }
-        g.sync();
-        // freeze at the cap or on a saturated link; compact the unfrozen list
-        int keep_n = 0;
-        bool froze = false;
-        for (int base = 0; base < nu; base += G::N) {
-          const int i = base + g.lane();
-          bool keep = false;
-          int p = 0;
-          if (i < nu) {
-            p = ul[i];
-            double cp = MF_INF;
-            if (has_caps) {
-              const double c0 = scap[p];
-              if (c0 < MF_INF) cp = smax(0.0, c0);
+        R = dadd(R, inc);
+        MF_TOC(OUT_CY_SUB + 2, q2);
+        MF_TIC(q3);
+        // residual update; saturated links collected, drained links dropped
+        int ns = 0, nt2 = 0;
+        for (int base = 0; base < nt; base += G::N) {
+          const int j = base + g.lane();
+          int l = 0, cn = 0;
+          bool sat = false, live = false;
+          if (j < nt) {
+            l = tl[j];
+            cn = cnt[l];
+            if (cn > 0) {
+              const double r = dsub(res[l], dmul(inc, (double)cn));
+              res[l] = r;
+              sat = r <= dmul(1e-12, capv[l]);
+              live = !sat;
             }
-            const double cap_eps = dmul(1e-12, smax(1.0, cp == MF_INF ? 0.0 : cp));
-            bool stop = rate[p] >= dsub(cp, cap_eps);
-            const int rn = arnp[p];
-            for (int k = 0; k < rn; ++k) {
-              const int l = arlp[p * RM + k];
-              if (res[l] <= dmul(1e-12, capv[l])) stop = true;
-            }
-            keep = !stop;
-            if (stop)  // a frozen member leaves every link count for good
-              for (int k = 0; k < rn; ++k) g.atomic_add(&cnt[arlp[p * RM + k]], -1);
           }
-          g.sync();  // every lane has read its entry before the in-place compaction
-          const unsigned m = g.ballot(keep);
-          if (keep) ul[keep_n + popc32(m & g.lanemask_lt())] = p;
-          keep_n += popc32(m);
-          if (i < nu && !keep) froze = true;
+          g.sync();  // all lanes read tl[j] before the in-place compaction
+          const unsigned ms = g.ballot(sat);
+          if (sat) I.s_sat[ns + popc32(ms & g.lanemask_lt())] = l;
+          ns += popc32(ms);
+          const unsigned ml = g.ballot(live);
+          if (live) tl[nt2 + popc32(ml & g.lanemask_lt())] = (unsigned short)l;
+          nt2 += popc32(ml);
         }
         g.sync();
-        bytes += (long long)nu * (20LL * RM + 29) + 32LL * nt;
-        if (!g.any(froze)) {
+        MF_TOC(OUT_CY_SUB + 3, q3);
+        MF_TIC(q4);
+        int frozen = 0;
+        // cap freezes: the unfrozen prefix of the cap order with cap - eps <= R
+        for (; cptr < ncap; ++cptr) {
+          const int p = (int)I.x_lo[cptr];
+          if (I.s_frz[p]) continue;
+          const double cp = bits_to_d(I.x_hi[cptr]);
+          const double cap_eps = dmul(1e-12, smax(1.0, cp));
+          if (!(R >= dsub(cp, cap_eps))) break;
+          freeze_member(p, R, RM);
+          ++frozen;
+        }
+        // link freezes: every unfrozen member of a saturated link
+        for (int q = 0; q < ns; ++q) frozen += freeze_link_members(I.s_sat[q], R, RM);
+        MF_TOC(OUT_CY_SUB + 4, q4);
+        bytes += 32LL * nt + 24LL * frozen;
+        if (frozen == 0) {
           fail(ERR_INTERNAL, CHK_NO_PROGRESS);
           return;
         }
-        nu = keep_n;
+        nu -= frozen;
+        nt = nt2;
       }
+      // any links still counting (none when every member froze) are cleared
+      for (int j = g.lane(); j < nt; j += G::N) cnt[tl[j]] = 0;
+      g.sync();
     }
     // restore l_res == capacity on every link a route of this step touched
+    MF_TIC(q5);
     for (int p = g.lane(); p < A; p += G::N) {
       const int rn = arnp[p];
       for (int k = 0; k < rn; ++k) {
@@ -1325,9 +1403,39 @@ struct Engine {
       }
     }
     g.sync();
+    MF_TOC(OUT_CY_SUB + 5, q5);
     s.classes += ncls;
     s.rounds += rounds;
     s.algo_bytes += bytes;
+  }
+
+  // a filled-class member freezes at rate R and leaves its links' counts
+  MF_FN void freeze_member(int p, double R, int RM) {
+    g.sync();
+    if (g.leader()) {
+      I.s_frz[p] = 1;
+      I.s_rate[p] = R;
+    }
+    const int rn = I.a_rn[p];
+    for (int k = g.lane(); k < rn; k += G::N) g.atomic_add(&I.l_cnt[I.a_rl[p * RM + k]], -1);
+    g.sync();
+  }
+  MF_FN int freeze_link_members(int l, double R, int RM) {
+    const int e0 = I.l_mb[l], e1 = I.l_off[l];
+    int got = 0;
+    for (int e = e0 + g.lane(); e < e1; e += G::N) {
+      const int p = I.s_mem[e];
+      if (g.atomic_exch_u8(&I.s_frz[p]) == 0) {
+        I.s_rate[p] = R;
+        const int rn = I.a_rn[p];
+        for (int k = 0; k < rn; ++k) g.atomic_add(&I.l_cnt[I.a_rl[p * RM + k]], -1);
+        ++got;
+      }
+    }
+    g.sync();
+    int tot = 0;
+    g.excl_scan(got, &tot);
+    return tot;
   }
 
   // engine.cpp:278-293
@@ -1351,6 +1459,13 @@ struct Engine {
     const double* __restrict__ rem = I.a_rem;
     double* __restrict__ evt = I.a_evt;
     unsigned long long* __restrict__ evs = I.a_evseq;
+    if (kOnChip) {
+      MF_SH(nr);
+      MF_SH(rt);
+      MF_SH(rem);
+      MF_SH(evt);
+      MF_SH(evs);
+    }
     int pushed = 0;
     for (int base = 0; base < A; base += G::N) {
       const int p = base + g.lane();
@@ -1503,6 +1618,11 @@ struct Engine {
   }
 
   MF_NOINLINE void release_flow(int fid) {  // engine.cpp:295-316
+    MF_TIC(rf);
+    release_flow_(fid);
+    MF_TOC(OUT_CY_SUB + 7, rf);
+  }
+  MF_FN void release_flow_(int fid) {
     if (I.f_state[fid] != FL_PENDING) {
       fail(ERR_INTERNAL, CHK_RELEASED_TWICE);
       return;
@@ -2299,7 +2419,7 @@ struct Engine {
     }
     recompute_rates();
     s.dirty = 0;
-    for (int k = 0; k < 8; ++k) s.cy[k] = 0;
+    for (int k = 0; k < 32; ++k) s.cy[k] = 0;
     while (!s.err) {
       MF_TIC(tn);
       Ev e = next_event();
@@ -2342,27 +2462,39 @@ struct Engine {
       }
       MF_TIC(th);
       switch (kind) {
-        case EV_FLOW:
+        case EV_FLOW: {
+          MF_TIC(h0);
           finish_flow(a);
+          MF_TOC(OUT_CY_SUB + 6, h0);
           break;
-        case EV_COMPUTE:
+        }
+        case EV_COMPUTE: {
+          MF_TIC(h1);
           handle_compute_complete(a, b);
+          MF_TOC(OUT_CY_SUB + 8, h1);
           break;
-        case EV_DEPART:
+        }
+        case EV_DEPART: {
+          MF_TIC(h2);
           handle_batch_depart(a);
+          MF_TOC(OUT_CY_SUB + 9, h2);
           break;
+        }
         case EV_ARRIVAL: {
           const int u = I.r_unit[a];
           put(&I.q_tail[u], I.q_tail[u] + 1);
           push(s.now, EV_ADMIT, u, -1);
           break;
         }
-        case EV_ADMIT:
+        case EV_ADMIT: {
+          MF_TIC(h3);
           if (I.p.workload_mode)
             handle_admit_try(a);
           else
             activate_manual_batch(a);
+          MF_TOC(OUT_CY_SUB + 10, h3);
           break;
+        }
         case EV_RELEASE:
           if (I.f_state[a] == FL_PENDING) release_flow(a);
           break;
@@ -2399,7 +2531,7 @@ struct Engine {
       I.out[OUT_NOW_BITS] = (long long)dbits(s.now);
       I.out[OUT_CLASSES] = s.classes;
       I.out[OUT_ROUNDS] = s.rounds;
-      for (int k = 0; k < 8; ++k) I.out[OUT_CY_NEXT + k] = s.cy[k];
+      for (int k = 0; k < 32; ++k) I.out[OUT_CY_NEXT + k] = s.cy[k];
     }
     g.sync();
   }

@@ -112,8 +112,15 @@ __global__ void __launch_bounds__(32)
       }
     }
     __syncwarp();
-    Engine<WarpLanes> eng(*d);
-    eng.run();
+    const bool on_chip = d->A_cap <= plan.AS && d->rmax <= plan.RM;
+    const bool links_on_chip = plan.NL > 0 && d->nlinks <= plan.NL;
+    if (on_chip && links_on_chip) {
+      Engine<WarpLanes, true, true> eng(*d);
+      eng.run();
+    } else {
+      Engine<WarpLanes, false, false> eng(*d);
+      eng.run();
+    }
     __syncwarp();
   }
 }

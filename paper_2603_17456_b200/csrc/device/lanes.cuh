@@ -55,6 +55,13 @@ struct WarpLanes {
   MF_FN int sum(int v) const { return __reduce_add_sync(0xffffffffu, (unsigned)v); }
   MF_FN int atomic_add(int* p, int v) const { return atomicAdd(p, v); }
   MF_FN unsigned atomic_or(unsigned* p, unsigned v) const { return atomicOr(p, v); }
+  // set a byte flag to 1, returning its previous value (32-bit CAS on the word)
+  MF_FN int atomic_exch_u8(uint8_t* p) const {
+    unsigned* w = reinterpret_cast<unsigned*>(reinterpret_cast<uintptr_t>(p) & ~uintptr_t(3));
+    const unsigned sh = (unsigned)(reinterpret_cast<uintptr_t>(p) & 3) * 8u;
+    const unsigned old = atomicOr(w, 1u << sh);
+    return (old >> sh) & 0xffu;
+  }
   // exclusive prefix sum of v over lanes; *total receives the warp sum
   MF_FN int excl_scan(int v, int* total) const {
     int x = v;
@@ -95,6 +102,11 @@ struct SerialLanes {
   inline unsigned atomic_or(unsigned* p, unsigned v) const {
     unsigned o = *p;
     *p = o | v;
+    return o;
+  }
+  inline int atomic_exch_u8(uint8_t* p) const {
+    int o = *p;
+    *p = 1;
     return o;
   }
   inline int excl_scan(int v, int* total) const {

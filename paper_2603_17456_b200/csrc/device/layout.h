@@ -207,6 +207,10 @@ struct Inst {
   int* s_ord;       // class order (active positions)
   int* s_cls;       // class start offsets (+1 sentinel)
   int* s_ul;        // unfrozen members of the class being filled
+  int* s_mem;       // link -> member incidence of that class [A_cap * rmax]
+  uint8_t* s_frz;   // member frozen flags (by active position)
+  int* s_sat;       // links saturated this round
+  int* l_mb;        // start of each link's member list in s_mem
   unsigned short* s_tl;  // links touched by that class [nlinks]
   int* srt;         // sorted-subset order of the last decide (flow ids)
   int* srt_add;     // flows released since the last decide
@@ -282,7 +286,10 @@ enum : int {
   OUT_CY_RESCHED,
   OUT_CY_BATCHEV,
   OUT_CY_PROMOTE,
-  OUT_N = 24
+  // sub-phases: allocate prep / count / inc / apply / freeze / restore,
+  // finish_flow, release_flow, compute-complete, depart, admit
+  OUT_CY_SUB = 24,
+  OUT_N = 48
 };
 
 }  // namespace mfb

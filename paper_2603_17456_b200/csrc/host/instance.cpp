@@ -675,6 +675,10 @@ void carve_instance(Carver& c, const InstanceInput& in, Inst& d, const Inst& top
   d.s_ord = c.S<int>(2 * pA);
   d.s_cls = c.S<int>(nA + 1);
   d.s_ul = c.S<int>(nA);
+  d.s_mem = c.S<int>(nA * d.rmax);
+  d.s_frz = c.S<uint8_t>(nA);
+  d.s_sat = c.S<int>(nl);
+  d.l_mb = c.S<int>(nl);
   d.s_tl = c.S<unsigned short>(nl);
   d.srt = c.S<int>(nA);
   d.srt_add = c.S<int>(nA);

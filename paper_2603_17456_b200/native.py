@@ -283,8 +283,8 @@ class DeviceBatch:
         return r
 
     def counters(self, i: int) -> np.ndarray:
-        out = np.zeros(32, np.int64)
-        n = self.n.lib.mfsim_dev_counters(self.h, i, _ptr(out), 32)
+        out = np.zeros(64, np.int64)
+        n = self.n.lib.mfsim_dev_counters(self.h, i, _ptr(out), 64)
         return out[:max(n, 0)]
 
     def raise_for_status(self, i: int):
