@@ -844,6 +844,44 @@ struct Engine {
       }
     }
   }
+  // ascending (x_hi, x_lo) order of n <= 128 entries: each lane holds up to
+  // four keys in registers and counts smaller keys over the warp (keys are
+  // unique: positions break ties); larger n use the bitonic sort_x
+  MF_FN void sort_caps(int n) {
+    if (n > 4 * G::N) {
+      sort_x(n);
+      return;
+    }
+    unsigned long long kh[4], kl[4];
+    int rk[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const int j = t * G::N + g.lane();
+      kh[t] = j < n ? I.x_hi[j] : ~0ull;
+      kl[t] = j < n ? I.x_lo[j] : ~0ull;
+      rk[t] = 0;
+    }
+#pragma unroll
+    for (int t2 = 0; t2 < 4; ++t2) {
+      for (int jj = 0; jj < G::N; ++jj) {
+        const unsigned long long oh = g.shfl(kh[t2], jj);
+        const unsigned long long ol = g.shfl(kl[t2], jj);
+#pragma unroll
+        for (int t = 0; t < 4; ++t) rk[t] += (oh < kh[t] || (oh == kh[t] && ol < kl[t])) ? 1 : 0;
+      }
+    }
+    g.sync();
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const int j = t * G::N + g.lane();
+      if (j < n) {
+        I.x_hi[rk[t]] = kh[t];
+        I.x_lo[rk[t]] = kl[t];
+      }
+    }
+    g.sync();
+  }
+
   // joint sort of x_hi/x_lo/x_val by (hi, lo)
   MF_FN void sort_x(int n) {
     if (n <= 1) return;
@@ -1177,7 +1215,202 @@ struct Engine {
   // number of unfrozen members per link, maintained incrementally (members
   // freeze permanently), which equals the reference's per-round recount; the
   // rounds then touch only that class's links and its unfrozen members.
-  MF_NOINLINE void allocate(int ncls, bool has_caps) {
+  MF_FN void allocate(int ncls, bool has_caps) {
+    if (kOnChip && kLinksOnChip)
+      allocate_chip(ncls, has_caps);
+    else
+      allocate_generic(ncls, has_caps);
+  }
+
+  // per-member rounds over global-memory arrays (instances beyond the
+  // shared-memory plan)
+  MF_NOINLINE void allocate_generic(int ncls, bool has_caps) {
+    const int A = s.n_active;
+    const int RM = I.rmax;
+    int* __restrict__ ord = I.s_ord;
+    const int* __restrict__ afid = I.a_fid;
+    const unsigned short* __restrict__ arlp = I.a_rl;
+    const uint8_t* __restrict__ arnp = I.a_rn;
+    double* __restrict__ res = I.l_res;
+    int* __restrict__ cnt = I.l_cnt;
+    double* __restrict__ rate = I.s_rate;
+    int* __restrict__ ul = I.s_ul;
+    unsigned short* __restrict__ tl = I.s_tl;
+    const double* __restrict__ capv = I.cap;
+    const double* __restrict__ scap = I.s_cap;
+    // rate-map insertion order for the load_fraction hash emulation
+    {
+      int* __restrict__ hk = I.h_keys;
+      int* __restrict__ hidx = I.f_hidx;
+      for (int i = g.lane(); i < A; i += G::N) {
+        const int fid = afid[ord[i]];
+        hk[i] = fid;
+        hidx[fid] = i;
+      }
+    }
+    g.sync();
+    s.h_n = A;
+    s.h_ready = 0;
+    long long rounds = 0, bytes = 0;
+    for (int c = 0; c < ncls; ++c) {
+      const int o0 = I.s_cls[c], o1 = I.s_cls[c + 1];
+      const int n = o1 - o0;
+      if (n == 1) {  // singleton: bottleneck residual, capped (allocator.cpp:42-59)
+        const int p = ord[o0];
+        const int rn = arnp[p];
+        double r = MF_INF;
+        if (has_caps) {
+          const double cp = scap[p];
+          if (cp < MF_INF) r = smax(0.0, cp);
+        }
+        double mine = MF_INF;
+        for (int k = g.lane(); k < rn; k += G::N) mine = smin(mine, smax(0.0, res[arlp[p * RM + k]]));
+        for (int m = G::N / 2; m > 0; m >>= 1) mine = smin(mine, g.shfl_xor(mine, m));
+        r = smin(r, mine);
+        g.sync();
+        for (int k = g.lane(); k < rn; k += G::N) {
+          const int l = arlp[p * RM + k];
+          res[l] = dsub(res[l], r);
+        }
+        if (g.leader()) rate[p] = r;
+        g.sync();
+        bytes += 20LL * rn + 12;
+        continue;
+      }
+      // multi-flow class: members start unfrozen at rate 0; count per link
+      int nt = 0;
+      for (int base = 0; base < n; base += G::N) {
+        const int i = base + g.lane();
+        int p = 0, rn = 0;
+        if (i < n) {
+          p = ord[o0 + i];
+          rn = arnp[p];
+          rate[p] = 0.0;
+          ul[i] = p;
+        }
+        for (int k = 0; k < RM; ++k) {
+          bool first = false;
+          int l = 0;
+          if (k < rn) {
+            l = arlp[p * RM + k];
+            first = g.atomic_add(&cnt[l], 1) == 0;
+          }
+          const unsigned m = g.ballot(first);
+          if (first) tl[nt + popc32(m & g.lanemask_lt())] = (unsigned short)l;
+          nt += popc32(m);
+        }
+      }
+      g.sync();
+      int nu = n;
+      while (nu > 0) {
+        ++rounds;
+        // inc = min over touched links of max(0, residual) / count and cap gaps.
+        // The exact quotients are only needed near the minimum: res * (1/cnt)
+        // is within 2 ulp of the correctly rounded res / cnt, so every link
+        // whose exact quotient can be the minimum lies within that margin of
+        // the approximate minimum; only those are divided exactly.
+        double amin = MF_INF;
+#pragma unroll 4
+        for (int j = g.lane(); j < nt; j += G::N) {
+          const int l = tl[j];
+          const int cn = cnt[l];
+          const double r = res[l];
+          if (cn > 0) amin = smin(amin, dmul(smax(0.0, r), recip(cn)));
+        }
+        double cmin = MF_INF;
+        if (has_caps) {
+#pragma unroll 4
+          for (int i = g.lane(); i < nu; i += G::N) {
+            const int p = ul[i];
+            const double cp = scap[p];
+            if (cp < MF_INF) cmin = smin(cmin, dsub(smax(0.0, cp), rate[p]));
+          }
+        }
+        for (int m = G::N / 2; m > 0; m >>= 1) {
+          amin = smin(amin, g.shfl_xor(amin, m));
+          cmin = smin(cmin, g.shfl_xor(cmin, m));
+        }
+        const double athr = dadd(amin, dmul(amin, 0x1p-44));
+        double inc = cmin;
+        if (amin <= cmin) {  // a link share may be the minimum: exact quotients near it
+#pragma unroll 4
+          for (int j = g.lane(); j < nt; j += G::N) {
+            const int l = tl[j];
+            const int cn = cnt[l];
+            const double r = smax(0.0, res[l]);
+            if (cn > 0 && dmul(r, recip(cn)) <= athr) inc = smin(inc, ddiv(r, (double)cn));
+          }
+          for (int m = G::N / 2; m > 0; m >>= 1) inc = smin(inc, g.shfl_xor(inc, m));
+        }
+        inc = smax(inc, 0.0);
+#pragma unroll 4
+        for (int i = g.lane(); i < nu; i += G::N) {
+          const int p = ul[i];
+          rate[p] = dadd(rate[p], inc);
+        }
+#pragma unroll 4
+        for (int j = g.lane(); j < nt; j += G::N) {
+          const int l = tl[j];
+          const int cn = cnt[l];
+          if (cn > 0) res[l] = dsub(res[l], dmul(inc, (double)cn));
+        }
+        g.sync();
+        // freeze at the cap or on a saturated link; compact the unfrozen list
+        int keep_n = 0;
+        bool froze = false;
+        for (int base = 0; base < nu; base += G::N) {
+          const int i = base + g.lane();
+          bool keep = false;
+          int p = 0;
+          if (i < nu) {
+            p = ul[i];
+            double cp = MF_INF;
+            if (has_caps) {
+              const double c0 = scap[p];
+              if (c0 < MF_INF) cp = smax(0.0, c0);
+            }
+            const double cap_eps = dmul(1e-12, smax(1.0, cp == MF_INF ? 0.0 : cp));
+            bool stop = rate[p] >= dsub(cp, cap_eps);
+            const int rn = arnp[p];
+            for (int k = 0; k < rn; ++k) {
+              const int l = arlp[p * RM + k];
+              if (res[l] <= dmul(1e-12, capv[l])) stop = true;
+            }
+            keep = !stop;
+            if (stop)  // a frozen member leaves every link count for good
+              for (int k = 0; k < rn; ++k) g.atomic_add(&cnt[arlp[p * RM + k]], -1);
+          }
+          g.sync();  // every lane has read its entry before the in-place compaction
+          const unsigned m = g.ballot(keep);
+          if (keep) ul[keep_n + popc32(m & g.lanemask_lt())] = p;
+          keep_n += popc32(m);
+          if (i < nu && !keep) froze = true;
+        }
+        g.sync();
+        bytes += (long long)nu * (20LL * RM + 29) + 32LL * nt;
+        if (!g.any(froze)) {
+          fail(ERR_INTERNAL, CHK_NO_PROGRESS);
+          return;
+        }
+        nu = keep_n;
+      }
+    }
+    // restore l_res == capacity on every link a route of this step touched
+    for (int p = g.lane(); p < A; p += G::N) {
+      const int rn = arnp[p];
+      for (int k = 0; k < rn; ++k) {
+        const int l = arlp[p * RM + k];
+        res[l] = capv[l];
+      }
+    }
+    g.sync();
+    s.classes += ncls;
+    s.rounds += rounds;
+    s.algo_bytes += bytes;
+  }
+
+  // class filling with the shared class rate (hot arrays on chip)
+  MF_NOINLINE void allocate_chip(int ncls, bool has_caps) {
     const int A = s.n_active;
     const int RM = I.rmax;
     int* __restrict__ ord = I.s_ord;
@@ -1241,6 +1474,20 @@ struct Engine {
       //   since cap - 1e-12*max(1,cap) is increasing in cap) and members of
       //   links whose residual fell to <= 1e-12 * capacity.
       MF_TIC(q1);
+      unsigned short* __restrict__ mem = I.c_mem;
+      unsigned short* __restrict__ mb = I.c_mb;
+      unsigned short* __restrict__ mend = I.c_end;
+      unsigned short* __restrict__ sat = I.c_sat;
+      uint8_t* __restrict__ frz = I.c_frz;
+      if (kOnChip) {
+        MF_SH(mem);
+        MF_SH(frz);
+      }
+      if (kLinksOnChip) {
+        MF_SH(mb);
+        MF_SH(mend);
+        MF_SH(sat);
+      }
       int nt = 0;
       int ncap = 0;
       for (int base = 0; base < n; base += G::N) {
@@ -1250,7 +1497,7 @@ struct Engine {
         if (i < n) {
           p = ord[o0 + i];
           rn = arnp[p];
-          I.s_frz[p] = 0;
+          frz[p] = 0;
           if (has_caps) capped = scap[p] < MF_INF;
         }
         for (int k = 0; k < RM; ++k) {
@@ -1273,9 +1520,8 @@ struct Engine {
         ncap += popc32(mc);
       }
       g.sync();
-      // link -> member incidence: offsets from the counts, then fill
-      int* __restrict__ loff = I.l_off;
-      int* __restrict__ mem = I.s_mem;
+      // link -> member incidence: extents from the counts, then a stable fill
+      // (equal links within a chunk ranked by lane, so no 16-bit atomics)
       {
         int off = 0;
         for (int base = 0; base < nt; base += G::N) {
@@ -1288,23 +1534,35 @@ struct Engine {
           int tot;
           const int o = g.excl_scan(c0, &tot);
           if (j < nt) {
-            loff[l] = off + o;
-            I.l_mb[l] = off + o;
+            mb[l] = (unsigned short)(off + o);
+            mend[l] = (unsigned short)(off + o);
           }
           off += tot;
         }
         g.sync();
-        for (int i = g.lane(); i < n; i += G::N) {
-          const int p = ord[o0 + i];
-          const int rn = arnp[p];
-          for (int k = 0; k < rn; ++k) {
-            const int l = arlp[p * RM + k];
-            mem[g.atomic_add(&loff[l], 1)] = p;
+        for (int base = 0; base < n; base += G::N) {
+          const int i = base + g.lane();
+          int p = 0, rn = 0;
+          if (i < n) {
+            p = ord[o0 + i];
+            rn = arnp[p];
+          }
+          for (int k = 0; k < RM; ++k) {
+            const bool has = k < rn;
+            const int l = has ? (int)arlp[p * RM + k] : -1 - g.lane();
+            const unsigned peers = g.match_any(l);
+            int pos = 0;
+            if (has) {
+              pos = mend[l] + popc32(peers & g.lanemask_lt());
+              mem[pos] = (unsigned short)p;
+            }
+            g.sync();
+            if (has && (peers >> g.lane()) == 1u) mend[l] = (unsigned short)(pos + 1);
+            g.sync();
           }
         }
-        g.sync();  // l's members: [l_mb[l], loff[l])
       }
-      if (ncap > 1) sort_x(ncap);  // caps ascending (cap >= 0: bit order)
+      if (ncap > 1) sort_caps(ncap);  // caps ascending (cap >= 0: bit order)
       MF_TOC(OUT_CY_SUB + 1, q1);
       int nu = n;
       int cptr = 0;
@@ -1313,7 +1571,7 @@ struct Engine {
         ++rounds;
         MF_TIC(q2);
         // capmin over unfrozen capped members (frozen ones skipped lazily)
-        while (cptr < ncap && I.s_frz[(int)I.x_lo[cptr]]) ++cptr;
+        while (cptr < ncap && frz[(int)I.x_lo[cptr]]) ++cptr;
         const double cmin = cptr < ncap ? dsub(bits_to_d(I.x_hi[cptr]), R) : MF_INF;
         double amin = MF_INF;
 #pragma unroll 4
@@ -1344,21 +1602,21 @@ struct Engine {
         int ns = 0, nt2 = 0;
         for (int base = 0; base < nt; base += G::N) {
           const int j = base + g.lane();
-          int l = 0, cn = 0;
-          bool sat = false, live = false;
+          int l = 0;
+          bool st = false, live = false;
           if (j < nt) {
             l = tl[j];
-            cn = cnt[l];
+            const int cn = cnt[l];
             if (cn > 0) {
               const double r = dsub(res[l], dmul(inc, (double)cn));
               res[l] = r;
-              sat = r <= dmul(1e-12, capv[l]);
-              live = !sat;
+              st = r <= dmul(1e-12, capv[l]);
+              live = !st;
             }
           }
           g.sync();  // all lanes read tl[j] before the in-place compaction
-          const unsigned ms = g.ballot(sat);
-          if (sat) I.s_sat[ns + popc32(ms & g.lanemask_lt())] = l;
+          const unsigned ms = g.ballot(st);
+          if (st) sat[ns + popc32(ms & g.lanemask_lt())] = (unsigned short)l;
           ns += popc32(ms);
           const unsigned ml = g.ballot(live);
           if (live) tl[nt2 + popc32(ml & g.lanemask_lt())] = (unsigned short)l;
@@ -1371,15 +1629,40 @@ struct Engine {
         // cap freezes: the unfrozen prefix of the cap order with cap - eps <= R
         for (; cptr < ncap; ++cptr) {
           const int p = (int)I.x_lo[cptr];
-          if (I.s_frz[p]) continue;
+          if (frz[p]) continue;
           const double cp = bits_to_d(I.x_hi[cptr]);
           const double cap_eps = dmul(1e-12, smax(1.0, cp));
           if (!(R >= dsub(cp, cap_eps))) break;
-          freeze_member(p, R, RM);
+          g.sync();
+          if (g.leader()) {
+            frz[p] = 1;
+            rate[p] = R;
+          }
+          const int rn = arnp[p];
+          for (int k = g.lane(); k < rn; k += G::N) g.atomic_add(&cnt[arlp[p * RM + k]], -1);
+          g.sync();
           ++frozen;
         }
-        // link freezes: every unfrozen member of a saturated link
-        for (int q = 0; q < ns; ++q) frozen += freeze_link_members(I.s_sat[q], R, RM);
+        // link freezes: every unfrozen member of a saturated link (links one
+        // after another; a link lists each member once)
+        for (int q = 0; q < ns; ++q) {
+          const int l = sat[q];
+          const int e0 = mb[l], e1 = mend[l];
+          int got = 0;
+          for (int e = e0 + g.lane(); e < e1; e += G::N) {
+            const int p = mem[e];
+            if (frz[p]) continue;
+            frz[p] = 1;
+            rate[p] = R;
+            const int rn = arnp[p];
+            for (int k = 0; k < rn; ++k) g.atomic_add(&cnt[arlp[p * RM + k]], -1);
+            ++got;
+          }
+          g.sync();
+          int tot;
+          g.excl_scan(got, &tot);
+          frozen += tot;
+        }
         MF_TOC(OUT_CY_SUB + 4, q4);
         bytes += 32LL * nt + 24LL * frozen;
         if (frozen == 0) {
@@ -1407,35 +1690,6 @@ struct Engine {
     s.classes += ncls;
     s.rounds += rounds;
     s.algo_bytes += bytes;
-  }
-
-  // a filled-class member freezes at rate R and leaves its links' counts
-  MF_FN void freeze_member(int p, double R, int RM) {
-    g.sync();
-    if (g.leader()) {
-      I.s_frz[p] = 1;
-      I.s_rate[p] = R;
-    }
-    const int rn = I.a_rn[p];
-    for (int k = g.lane(); k < rn; k += G::N) g.atomic_add(&I.l_cnt[I.a_rl[p * RM + k]], -1);
-    g.sync();
-  }
-  MF_FN int freeze_link_members(int l, double R, int RM) {
-    const int e0 = I.l_mb[l], e1 = I.l_off[l];
-    int got = 0;
-    for (int e = e0 + g.lane(); e < e1; e += G::N) {
-      const int p = I.s_mem[e];
-      if (g.atomic_exch_u8(&I.s_frz[p]) == 0) {
-        I.s_rate[p] = R;
-        const int rn = I.a_rn[p];
-        for (int k = 0; k < rn; ++k) g.atomic_add(&I.l_cnt[I.a_rl[p * RM + k]], -1);
-        ++got;
-      }
-    }
-    g.sync();
-    int tot = 0;
-    g.excl_scan(got, &tot);
-    return tot;
   }
 
   // engine.cpp:278-293

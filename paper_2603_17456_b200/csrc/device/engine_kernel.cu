@@ -40,6 +40,8 @@ __host__ inline SmemPlan make_plan(int rmax, int nlinks) {
   b += align16(p.AS * 8) + align16(p.AS * 4);                       // s_rate, s_ul
   b += align16(p.ES * 8) * 2 + align16(p.ES * 4) * 3;               // event pool
   b += align16(p.NL * 8) + align16(p.NL * 4) + align16(p.NL * 2);   // l_res, l_cnt, s_tl
+  b += align16(p.AS * p.RM * 2) + align16(p.AS + 4);                // c_mem, c_frz
+  b += 3 * align16(p.NL * 2);                                       // c_mb, c_end, c_sat
   p.bytes = align16(b);
   return p;
 }
@@ -105,10 +107,18 @@ __global__ void __launch_bounds__(32)
       } else {
         q += 2 * align16(plan.ES * 8) + 3 * align16(plan.ES * 4);
       }
+      const bool on_chip = d->A_cap <= plan.AS && d->rmax <= plan.RM;
       if (plan.NL > 0 && d->nlinks <= plan.NL) {
         d->l_res = reinterpret_cast<double*>(take(plan.NL * 8));
         d->l_cnt = reinterpret_cast<int*>(take(plan.NL * 4));
         d->s_tl = reinterpret_cast<unsigned short*>(take(plan.NL * 2));
+        if (on_chip) {
+          d->c_mem = reinterpret_cast<unsigned short*>(take(plan.AS * plan.RM * 2));
+          d->c_frz = reinterpret_cast<uint8_t*>(take(plan.AS + 4));
+          d->c_mb = reinterpret_cast<unsigned short*>(take(plan.NL * 2));
+          d->c_end = reinterpret_cast<unsigned short*>(take(plan.NL * 2));
+          d->c_sat = reinterpret_cast<unsigned short*>(take(plan.NL * 2));
+        }
       }
     }
     __syncwarp();

@@ -207,10 +207,13 @@ struct Inst {
   int* s_ord;       // class order (active positions)
   int* s_cls;       // class start offsets (+1 sentinel)
   int* s_ul;        // unfrozen members of the class being filled
-  int* s_mem;       // link -> member incidence of that class [A_cap * rmax]
-  uint8_t* s_frz;   // member frozen flags (by active position)
-  int* s_sat;       // links saturated this round
-  int* l_mb;        // start of each link's member list in s_mem
+  // on-chip class filling (engine allocate_chip): 16-bit link->member
+  // incidence of the class, per-link extents, saturated-link list, flags
+  unsigned short* c_mem;  // [A_cap * rmax]
+  unsigned short* c_mb;   // [nlinks] member list start
+  unsigned short* c_end;  // [nlinks] member list end / fill cursor
+  unsigned short* c_sat;  // [nlinks]
+  uint8_t* c_frz;         // [A_cap]
   unsigned short* s_tl;  // links touched by that class [nlinks]
   int* srt;         // sorted-subset order of the last decide (flow ids)
   int* srt_add;     // flows released since the last decide

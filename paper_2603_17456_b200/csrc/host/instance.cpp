@@ -2,6 +2,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <map>
@@ -509,6 +510,8 @@ void carve_instance(Carver& c, const InstanceInput& in, Inst& d, const Inst& top
     E = B * 3 + F + 64 + in.e_boost;
   }
   A = in.a_cap > 0 ? in.a_cap : std::min<long>(std::max<long>(F, 1), kSmemActive);
+  // test knob: exercise the global-memory variant of the engine
+  if (std::getenv("MFSIM_FORCE_GLOBAL") && A <= kSmemActive) A = kSmemActive + 1;
   A = std::max<long>(A, 1);
   const long X = A * d.rmax;
   const int LR = t.lr_cap;
@@ -675,10 +678,11 @@ void carve_instance(Carver& c, const InstanceInput& in, Inst& d, const Inst& top
   d.s_ord = c.S<int>(2 * pA);
   d.s_cls = c.S<int>(nA + 1);
   d.s_ul = c.S<int>(nA);
-  d.s_mem = c.S<int>(nA * d.rmax);
-  d.s_frz = c.S<uint8_t>(nA);
-  d.s_sat = c.S<int>(nl);
-  d.l_mb = c.S<int>(nl);
+  d.c_mem = c.S<unsigned short>(nA * d.rmax);
+  d.c_mb = c.S<unsigned short>(nl);
+  d.c_end = c.S<unsigned short>(nl);
+  d.c_sat = c.S<unsigned short>(nl);
+  d.c_frz = c.S<uint8_t>(nA + 4);
   d.s_tl = c.S<unsigned short>(nl);
   d.srt = c.S<int>(nA);
   d.srt_add = c.S<int>(nA);

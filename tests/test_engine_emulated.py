@@ -25,3 +25,22 @@ def test_livelock_error_code(emu):
     with pytest.raises(MfsimError) as e:
         run_manual(cases.livelock(), lib=emu)
     assert e.value.code == manifest()["errors"]["livelock"]
+
+
+GLOBAL_CASES = ["trio_karuna", "egress_mfs", "tick_promotion", "soft_enforcement_on", "random_004",
+                "random_013", "rli_007"]
+
+
+@pytest.mark.parametrize("name", GLOBAL_CASES)
+def test_global_memory_variant_manual(emu, name, monkeypatch):
+    """instances beyond the shared-memory plan take the generic engine variant"""
+    monkeypatch.setenv("MFSIM_FORCE_GLOBAL", "1")
+    res = run_manual(cases.manual_cases()[name], lib=emu)
+    assert mismatches(res, "manual", name) == []
+
+
+@pytest.mark.parametrize("name", ["example_karuna", "sanity_mfs", "fattree_sjf", "cluster8_400_edf"])
+def test_global_memory_variant_workload(emu, name, monkeypatch):
+    monkeypatch.setenv("MFSIM_FORCE_GLOBAL", "1")
+    res = run_config(cases.workload_cases()[name], lib=emu)
+    assert mismatches(res, "workload", name) == []
