@@ -97,9 +97,14 @@ class Clocks:
 
 
 def cells_for(rank: int, world: int, n: int, step_offset: int = 0):
+    """rank's slice of the sweep: consecutive chunks of a fixed shuffle of the
+    11,200 cells, so every step mixes loads, SLO scales, seeds and policies"""
+    import random
+
     from paper_2603_17456_b200 import sweep
 
     allc = sweep.sweep_cells()
+    random.Random(2603).shuffle(allc)
     start = ((step_offset * world + rank) * n) % len(allc)
     return [allc[(start + i) % len(allc)] for i in range(n)]
 
@@ -215,7 +220,8 @@ def main():
     from paper_2603_17456_b200.native import DeviceBatch, product
 
     lib = product()
-    stream = torch.cuda.current_stream()
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
     cells = cells_for(rank, world, args.instances)
     t0 = time.perf_counter()
     batch = DeviceBatch(local, lib, stream=stream.cuda_stream)

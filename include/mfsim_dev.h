@@ -55,7 +55,7 @@ typedef struct mfsim_dev_stats {
 /* create a context on CUDA device `device` */
 int mfsim_dev_create(int device, mfsim_dev** out);
 void mfsim_dev_destroy(mfsim_dev* d);
-/* run on the caller's cudaStream_t (NULL = the context's own stream) */
+/* run on the caller's cudaStream_t (NULL = the legacy default stream) */
 int mfsim_dev_set_stream(mfsim_dev* d, void* cuda_stream);
 
 /* queue one workload-mode instance from a config (policy, fabric, workload) */

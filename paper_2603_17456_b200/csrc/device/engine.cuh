@@ -151,6 +151,7 @@ struct Sc {
   int err, chk;
   long long pruned;
   int max_active;
+  int max_touch, max_pool;
   long long cy[32];
 };
 
@@ -237,6 +238,7 @@ struct Engine {
     ++s.n_ev;
     ++s.seq;
     ++s.pushes;
+    if (s.n_ev > s.max_pool) s.max_pool = s.n_ev;
   }
 
   // K4: the earliest of the arrival head, the event pool and the per-flow
@@ -1564,6 +1566,7 @@ struct Engine {
       }
       if (ncap > 1) sort_caps(ncap);  // caps ascending (cap >= 0: bit order)
       MF_TOC(OUT_CY_SUB + 1, q1);
+      if (nt > s.max_touch) s.max_touch = nt;
       int nu = n;
       int cptr = 0;
       double R = 0.0;
@@ -2656,6 +2659,8 @@ struct Engine {
     s.chk = 0;
     s.pruned = 0;
     s.max_active = 0;
+    s.max_touch = 0;
+    s.max_pool = 0;
     s.horizon = I.p.horizon;
     s.n_srt = 0;
     s.n_add = 0;
@@ -2785,6 +2790,8 @@ struct Engine {
       I.out[OUT_NOW_BITS] = (long long)dbits(s.now);
       I.out[OUT_CLASSES] = s.classes;
       I.out[OUT_ROUNDS] = s.rounds;
+      I.out[OUT_MAXTOUCH] = s.max_touch;
+      I.out[OUT_MAXPOOL] = s.max_pool;
       for (int k = 0; k < 32; ++k) I.out[OUT_CY_NEXT + k] = s.cy[k];
     }
     g.sync();

@@ -212,7 +212,8 @@ class CudaBackend final : public Backend {
       timed_ = false;
     }
   }
-  void set_stream(void* s) override { stream_ = s ? static_cast<cudaStream_t>(s) : own_; }
+  // any caller stream, including 0 (the legacy default stream)
+  void set_stream(void* s) override { stream_ = static_cast<cudaStream_t>(s); }
   double last_kernel_ms() const override { return last_ms_; }
   int kernel_launches() const override { return launches_; }
 

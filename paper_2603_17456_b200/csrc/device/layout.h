@@ -280,6 +280,8 @@ enum : int {
   OUT_NOW_BITS,
   OUT_CLASSES,
   OUT_ROUNDS,
+  OUT_MAXTOUCH,  // most links touched by one filled class
+  OUT_MAXPOOL,   // deepest event pool
   // phase cycle counters (profiling builds, -DMF_PROF)
   OUT_CY_NEXT = 16,
   OUT_CY_ADVANCE,
