@@ -147,6 +147,9 @@ struct Sc {
   int n_live;
   int h_n, h_ready;
   int n_srt, n_add;
+  int n_slots;
+  bool bk_slots;
+  int bk_n;
   int dirty;
   int err, chk;
   long long pruned;
@@ -177,8 +180,8 @@ MF_FN bool ev_less(const Ev& x, const Ev& y) {
   return x.seq < y.seq;
 }
 
-// kOnChip: active-flow arrays staged in shared memory; kLinksOnChip: per-link
-// residual / count arrays staged too (the common case; see engine_kernel.cu).
+// kLinksOnChip: the link -> slot map and the per-slot filling state were
+// staged in shared memory by the kernel (see engine_kernel.cu make_plan).
 template <class G, bool kOnChip = false, bool kLinksOnChip = false>
 struct Engine {
   G g;
@@ -251,10 +254,6 @@ struct Engine {
     const int* __restrict__ ek = I.e_kind;
     const double* __restrict__ at = I.a_evt;
     const unsigned long long* __restrict__ as = I.a_evseq;
-    if (kOnChip) {
-      MF_SH(at);
-      MF_SH(as);
-    }
     double bt = MF_INF;
     unsigned long long bk = ~0ull;
     int bsi = 0;  // (src << 28) | idx, src 0 = none
@@ -353,10 +352,6 @@ struct Engine {
       const int na = s.n_active;
       double* __restrict__ rem = I.a_rem;
       const double* __restrict__ rt = I.a_rate;
-      if (kOnChip) {
-        MF_SH(rem);
-        MF_SH(rt);
-      }
       bool bad = false;
 #pragma unroll 4
       for (int p = g.lane(); p < na; p += G::N) {
@@ -445,9 +440,73 @@ struct Engine {
   // Stable bucketing by link of n entries (link x_seg[e], key x_hi[e], value
   // x_val[e]) into y_key / y_val: a warp counting sort whose scatter ranks
   // equal links by lane (match_any), so each link's bucket keeps entry order.
-  // On return l_cnt[l] = bucket size, l_off[l] = bucket end for the touched
-  // links s_tl[0, nt); release() must zero l_cnt again.
+  // The buckets of the distinct links are addressed through compact slots
+  // (l2s map + sl_cnt / sl_mb / sl_end, on chip) when they fit TS_cap, else
+  // through the per-link arrays (l_cnt / l_off). Query a link's bucket with
+  // bucket_of(); bucket_release() clears the state.
   MF_FN int bucket_by_link(int n) {
+    s.bk_slots = false;
+    if (I.TS_cap > 0) {
+      // claim a slot per distinct link
+      unsigned short* __restrict__ l2s = I.l2s;
+      int ns = 0;
+      for (int base = 0; base < n; base += G::N) {
+        const int e = base + g.lane();
+        const bool has = e < n;
+        const int l = has ? I.x_seg[e] : -1 - g.lane();
+        const unsigned peers = g.match_any(l);
+        const bool fresh = has && (peers & g.lanemask_lt()) == 0u && l2s[l] == 0xFFFFu;
+        const unsigned m = g.ballot(fresh);
+        if (fresh) {
+          const int sl = ns + popc32(m & g.lanemask_lt());
+          l2s[l] = (unsigned short)(sl < I.TS_cap ? sl : 0xFFFEu);
+          if (sl < I.TS_cap) {
+            I.sl_link[sl] = (unsigned short)l;
+            I.sl_cnt[sl] = 0;
+          }
+          I.x_lo[sl] = (unsigned long long)l;  // claimed links (for the overflow reset)
+        }
+        ns += popc32(m);
+        g.sync();
+      }
+      if (ns <= I.TS_cap) {
+        s.bk_slots = true;
+        s.bk_n = ns;
+        for (int e = g.lane(); e < n; e += G::N) g.atomic_add(&I.sl_cnt[l2s[I.x_seg[e]]], 1);
+        g.sync();
+        int off = 0;
+        for (int base = 0; base < ns; base += G::N) {
+          const int j = base + g.lane();
+          const int c = j < ns ? I.sl_cnt[j] : 0;
+          int tot;
+          const int o = g.excl_scan(c, &tot);
+          if (j < ns) {
+            I.sl_mb[j] = (unsigned short)(off + o);
+            I.sl_end[j] = (unsigned short)(off + o);
+          }
+          off += tot;
+        }
+        g.sync();
+        for (int base = 0; base < n; base += G::N) {
+          const int e = base + g.lane();
+          const int sl = e < n ? (int)l2s[I.x_seg[e]] : -1 - g.lane();
+          const unsigned peers = g.match_any(sl);
+          int pos = 0;
+          if (e < n) {
+            pos = I.sl_end[sl] + popc32(peers & g.lanemask_lt());
+            I.y_key[pos] = I.x_hi[e];
+            I.y_val[pos] = I.x_val[e];
+          }
+          g.sync();
+          if (e < n && (peers >> g.lane()) == 1u) I.sl_end[sl] = (unsigned short)(pos + 1);
+          g.sync();
+        }
+        return ns;
+      }
+      for (int j = g.lane(); j < ns; j += G::N) l2s[(int)I.x_lo[j]] = 0xFFFFu;
+      g.sync();
+    }
+    // per-link global arrays
     int nt = 0;
     for (int base = 0; base < n; base += G::N) {
       const int e = base + g.lane();
@@ -489,10 +548,42 @@ struct Engine {
       if (e < n && (peers >> g.lane()) == 1u) I.l_off[l] += popc32(peers);
       g.sync();
     }
+    s.bk_n = nt;
     return nt;
   }
+  // j-th bucketed link and its entry range [*e0, *e1)
+  MF_FN int bucket_at(int j, int* e0, int* e1) const {
+    if (s.bk_slots) {
+      *e0 = I.sl_mb[j];
+      *e1 = I.sl_end[j];
+      return I.sl_link[j];
+    }
+    const int l = I.s_tl[j];
+    *e1 = I.l_off[l];
+    *e0 = *e1 - I.l_cnt[l];
+    return l;
+  }
+  // entry range of link l (empty when l has no entries)
+  MF_FN bool bucket_of(int l, int* e0, int* e1) const {
+    if (s.bk_slots) {
+      const int sl = I.l2s[l];
+      if (sl == 0xFFFF) return false;
+      *e0 = I.sl_mb[sl];
+      *e1 = I.sl_end[sl];
+      return true;
+    }
+    const int c = I.l_cnt[l];
+    if (c == 0) return false;
+    *e1 = I.l_off[l];
+    *e0 = *e1 - c;
+    return true;
+  }
   MF_FN void bucket_release(int nt) {
-    for (int j = g.lane(); j < nt; j += G::N) I.l_cnt[I.s_tl[j]] = 0;
+    if (s.bk_slots) {
+      for (int j = g.lane(); j < nt; j += G::N) I.l2s[I.sl_link[j]] = 0xFFFFu;
+    } else {
+      for (int j = g.lane(); j < nt; j += G::N) I.l_cnt[I.s_tl[j]] = 0;
+    }
     g.sync();
   }
 
@@ -527,8 +618,8 @@ struct Engine {
     const int nt = bucket_by_link(n);
     // per link: insertion sort by (key, rate), then running sums in that order
     for (int j = g.lane(); j < nt; j += G::N) {
-      const int l = I.s_tl[j];
-      const int e1 = I.l_off[l], e0 = e1 - I.l_cnt[l];
+      int e0, e1;
+      bucket_at(j, &e0, &e1);
       for (int a = e0 + 1; a < e1; ++a) {
         const unsigned long long k = I.y_key[a];
         const double v = I.y_val[a];
@@ -555,10 +646,9 @@ struct Engine {
 
   // LinkLoadIndex::higher_fraction (allocator.cpp:163-171); per-lane query
   MF_FN double index_fraction(int l, int band, int level) const {
-    const int cnt = I.l_cnt[l];
-    if (cnt == 0) return 0.0;
+    int e0, e1;
+    if (!bucket_of(l, &e0, &e1)) return 0.0;
     const unsigned long long want = ((unsigned long long)band << 16) | (unsigned long long)level;
-    const int e1 = I.l_off[l], e0 = e1 - cnt;
     int lo = e0, hi = e1;  // first entry with key >= want
     while (lo < hi) {
       const int mid = (lo + hi) >> 1;
@@ -1186,9 +1276,10 @@ struct Engine {
     }
     const int nt = bucket_by_link(n);
     for (int j = g.lane(); j < nt; j += G::N) {
-      const int l = I.s_tl[j];
-      const int e1 = I.l_off[l], e0 = e1 - I.l_cnt[l];
+      int e0, e1;
+      const int l = bucket_at(j, &e0, &e1);
       double dmd = 0.0;
+#pragma unroll 4
       for (int a = e0; a < e1; ++a) dmd = dadd(dmd, I.y_val[a]);
       I.l_x[l] = dmd;
     }
@@ -1218,10 +1309,55 @@ struct Engine {
   // freeze permanently), which equals the reference's per-round recount; the
   // rounds then touch only that class's links and its unfrozen members.
   MF_FN void allocate(int ncls, bool has_caps) {
-    if (kOnChip && kLinksOnChip)
-      allocate_chip(ncls, has_caps);
+    if (I.TS_cap > 0 && build_slots())
+      allocate_slots(ncls, has_caps);
     else
       allocate_generic(ncls, has_caps);
+  }
+
+  // Compact slots for the links of every active route (this step): a slot per
+  // distinct link, residual initialised to the capacity (allocator.cpp:36-37).
+  // Returns false (and leaves l2s clear) when they exceed TS_cap.
+  MF_NOINLINE bool build_slots() {
+    const int A = s.n_active;
+    const int RM = I.rmax;
+    unsigned short* __restrict__ l2s = I.l2s;
+    unsigned short* __restrict__ asl = I.a_sl;
+    int* __restrict__ claimed = I.x_seg;  // every claimed link, for the reset
+    int ns = 0;
+    for (int base = 0; base < A; base += G::N) {
+      const int p = base + g.lane();
+      const int rn = p < A ? (int)I.a_rn[p] : 0;
+      for (int k = 0; k < RM; ++k) {
+        const bool has = k < rn;
+        const int l = has ? (int)I.a_rl[p * RM + k] : -1 - g.lane();
+        const unsigned peers = g.match_any(l);
+        const bool lead = has && (peers & g.lanemask_lt()) == 0u;
+        const bool fresh = lead && l2s[l] == 0xFFFFu;
+        const unsigned m = g.ballot(fresh);
+        if (fresh) {
+          const int sl = ns + popc32(m & g.lanemask_lt());
+          claimed[sl] = l;
+          l2s[l] = (unsigned short)(sl < I.TS_cap ? sl : 0xFFFEu);
+          if (sl < I.TS_cap) {
+            I.sl_link[sl] = (unsigned short)l;
+            I.sl_res[sl] = I.cap[l];
+            I.sl_cnt[sl] = 0;
+          }
+        }
+        ns += popc32(m);
+        g.sync();
+        if (has) asl[p * RM + k] = l2s[l];
+      }
+    }
+    g.sync();
+    if (ns > I.TS_cap) {
+      for (int j = g.lane(); j < ns; j += G::N) l2s[claimed[j]] = 0xFFFFu;
+      g.sync();
+      return false;
+    }
+    s.n_slots = ns;
+    return true;
   }
 
   // per-member rounds over global-memory arrays (instances beyond the
@@ -1411,20 +1547,21 @@ struct Engine {
     s.algo_bytes += bytes;
   }
 
-  // class filling with the shared class rate (hot arrays on chip)
-  MF_NOINLINE void allocate_chip(int ncls, bool has_caps) {
+  // class filling with the shared class rate over compact link slots
+  MF_NOINLINE void allocate_slots(int ncls, bool has_caps) {
     const int A = s.n_active;
     const int RM = I.rmax;
     int* __restrict__ ord = I.s_ord;
     const int* __restrict__ afid = I.a_fid;
-    const unsigned short* __restrict__ arlp = I.a_rl;
+    const unsigned short* __restrict__ arlp = I.a_sl;  // slot ids
     const uint8_t* __restrict__ arnp = I.a_rn;
-    double* __restrict__ res = I.l_res;
-    int* __restrict__ cnt = I.l_cnt;
+    double* __restrict__ res = I.sl_res;
+    int* __restrict__ cnt = I.sl_cnt;
     double* __restrict__ rate = I.s_rate;
     int* __restrict__ ul = I.s_ul;
-    unsigned short* __restrict__ tl = I.s_tl;
+    unsigned short* __restrict__ tl = I.sl_tl;
     const double* __restrict__ capv = I.cap;
+    const unsigned short* __restrict__ slink = I.sl_link;
     const double* __restrict__ scap = I.s_cap;
     MF_TIC(q0);
     // rate-map insertion order for the load_fraction hash emulation
@@ -1477,14 +1614,10 @@ struct Engine {
       //   links whose residual fell to <= 1e-12 * capacity.
       MF_TIC(q1);
       unsigned short* __restrict__ mem = I.c_mem;
-      unsigned short* __restrict__ mb = I.c_mb;
-      unsigned short* __restrict__ mend = I.c_end;
-      unsigned short* __restrict__ sat = I.c_sat;
+      unsigned short* __restrict__ mb = I.sl_mb;
+      unsigned short* __restrict__ mend = I.sl_end;
+      unsigned short* __restrict__ sat = I.sl_sat;
       uint8_t* __restrict__ frz = I.c_frz;
-      if (kOnChip) {
-        MF_SH(mem);
-        MF_SH(frz);
-      }
       if (kLinksOnChip) {
         MF_SH(mb);
         MF_SH(mend);
@@ -1613,7 +1746,7 @@ struct Engine {
             if (cn > 0) {
               const double r = dsub(res[l], dmul(inc, (double)cn));
               res[l] = r;
-              st = r <= dmul(1e-12, capv[l]);
+              st = r <= dmul(1e-12, capv[slink[l]]);
               live = !st;
             }
           }
@@ -1679,17 +1812,9 @@ struct Engine {
       for (int j = g.lane(); j < nt; j += G::N) cnt[tl[j]] = 0;
       g.sync();
     }
-    // restore l_res == capacity on every link a route of this step touched
-    MF_TIC(q5);
-    for (int p = g.lane(); p < A; p += G::N) {
-      const int rn = arnp[p];
-      for (int k = 0; k < rn; ++k) {
-        const int l = arlp[p * RM + k];
-        res[l] = capv[l];
-      }
-    }
+    // clear the link -> slot map for the next step
+    for (int j = g.lane(); j < s.n_slots; j += G::N) I.l2s[slink[j]] = 0xFFFFu;
     g.sync();
-    MF_TOC(OUT_CY_SUB + 5, q5);
     s.classes += ncls;
     s.rounds += rounds;
     s.algo_bytes += bytes;
@@ -1716,13 +1841,6 @@ struct Engine {
     const double* __restrict__ rem = I.a_rem;
     double* __restrict__ evt = I.a_evt;
     unsigned long long* __restrict__ evs = I.a_evseq;
-    if (kOnChip) {
-      MF_SH(nr);
-      MF_SH(rt);
-      MF_SH(rem);
-      MF_SH(evt);
-      MF_SH(evs);
-    }
     int pushed = 0;
     for (int base = 0; base < A; base += G::N) {
       const int p = base + g.lane();
@@ -2664,6 +2782,8 @@ struct Engine {
     s.horizon = I.p.horizon;
     s.n_srt = 0;
     s.n_add = 0;
+    s.n_slots = 0;
+    for (int l = g.lane(); l < I.nlinks; l += G::N) I.l2s[l] = 0xFFFFu;
     if (!I.host_init) {
       init_state();
     } else {

@@ -31,14 +31,8 @@ class EmuBackend final : public Backend {
   void launch(const mfb::Inst* d, const int*, int n, const LaunchHint&) override {
     for (int i = 0; i < n; ++i) {
       mfb::Inst local = d[i];
-      // same variant choice as the device kernel's shared-memory plan
-      if (local.A_cap <= kSmemActive && local.nlinks <= kSmemLinks) {
-        mfb::Engine<mfb::SerialLanes, true, true> eng(local);
-        eng.run();
-      } else {
-        mfb::Engine<mfb::SerialLanes, false, false> eng(local);
-        eng.run();
-      }
+      mfb::Engine<mfb::SerialLanes, false, false> eng(local);
+      eng.run();
     }
     ++launches_;
   }

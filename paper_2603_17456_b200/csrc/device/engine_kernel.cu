@@ -20,28 +20,27 @@ namespace mfb {
 // hot arrays of an instance whenever its capacities fit (active-flow state +
 // route cache + per-step rates, the event pool, per-link residual / count).
 struct SmemPlan {
-  int AS;  // active flows
-  int RM;  // route length stride
-  int ES;  // event pool
-  int NL;  // links
+  int ES;  // event pool entries
+  int NL;  // link -> slot map entries (0: map stays in global memory)
+  int TS;  // slots
   int bytes;
 };
 
 __host__ __device__ inline int align16(int x) { return (x + 15) & ~15; }
 
-__host__ inline SmemPlan make_plan(int rmax, int nlinks) {
+// Per-warp shared memory: the descriptor copy, the event pool, the link ->
+// slot map and the per-slot filling state. The active-flow arrays stay in
+// global memory (L1/L2): measured sweep instances reach 250-900 active flows,
+// and keeping shared memory small lets ~19 warps share an SM.
+__host__ inline SmemPlan make_plan(int nlinks) {
   SmemPlan p{};
-  p.AS = mfh::kSmemActive;
-  p.RM = rmax;
   p.ES = mfh::kSmemEvents;
   p.NL = nlinks <= mfh::kSmemLinks ? nlinks : 0;
+  p.TS = p.NL > 0 ? mfh::kSmemSlots : 0;
   int b = align16(sizeof(Inst));
-  b += align16(p.AS * 4) + 4 * align16(p.AS * 8) + align16(p.AS * p.RM * 2) + align16(p.AS);
-  b += align16(p.AS * 8) + align16(p.AS * 4);                       // s_rate, s_ul
-  b += align16(p.ES * 8) * 2 + align16(p.ES * 4) * 3;               // event pool
-  b += align16(p.NL * 8) + align16(p.NL * 4) + align16(p.NL * 2);   // l_res, l_cnt, s_tl
-  b += align16(p.AS * p.RM * 2) + align16(p.AS + 4);                // c_mem, c_frz
-  b += 3 * align16(p.NL * 2);                                       // c_mb, c_end, c_sat
+  b += align16(p.ES * 8) * 2 + align16(p.ES * 4) * 3;
+  b += align16(p.NL * 2);
+  b += align16(p.TS * 8) + align16(p.TS * 4) + 5 * align16(p.TS * 2);
   p.bytes = align16(b);
   return p;
 }
@@ -58,13 +57,13 @@ __global__ void __launch_bounds__(32)
     i = __shfl_sync(0xffffffffu, i, 0);
     if (i >= n) return;
     i = order[i];  // longest estimated instances first
-    // descriptor copy (8-byte words across the warp)
-    {
+    {  // descriptor copy (8-byte words across the warp)
       const unsigned long long* src = reinterpret_cast<const unsigned long long*>(insts + i);
       unsigned long long* dst = reinterpret_cast<unsigned long long*>(d);
       for (int w = lane; w < (int)(sizeof(Inst) / 8); w += 32) dst[w] = src[w];
     }
     __syncwarp();
+    bool slots_on_chip = false;
     if (lane == 0) {
       unsigned char* q = smem + align16(sizeof(Inst));
       auto take = [&](int bytes) {
@@ -72,20 +71,6 @@ __global__ void __launch_bounds__(32)
         q += align16(bytes);
         return r;
       };
-      if (d->A_cap <= plan.AS && d->rmax <= plan.RM) {
-        d->a_fid = reinterpret_cast<int*>(take(plan.AS * 4));
-        d->a_rem = reinterpret_cast<double*>(take(plan.AS * 8));
-        d->a_rate = reinterpret_cast<double*>(take(plan.AS * 8));
-        d->a_evt = reinterpret_cast<double*>(take(plan.AS * 8));
-        d->a_evseq = reinterpret_cast<unsigned long long*>(take(plan.AS * 8));
-        d->a_rl = reinterpret_cast<unsigned short*>(take(plan.AS * plan.RM * 2));
-        d->a_rn = reinterpret_cast<uint8_t*>(take(plan.AS));
-        d->s_rate = reinterpret_cast<double*>(take(plan.AS * 8));
-        d->s_ul = reinterpret_cast<int*>(take(plan.AS * 4));
-      } else {
-        q += align16(plan.AS * 4) + 4 * align16(plan.AS * 8) + align16(plan.AS * plan.RM * 2) +
-             align16(plan.AS) + align16(plan.AS * 8) + align16(plan.AS * 4);
-      }
       if (d->E_cap <= plan.ES) {
         double* et = reinterpret_cast<double*>(take(plan.ES * 8));
         unsigned long long* es = reinterpret_cast<unsigned long long*>(take(plan.ES * 8));
@@ -107,25 +92,23 @@ __global__ void __launch_bounds__(32)
       } else {
         q += 2 * align16(plan.ES * 8) + 3 * align16(plan.ES * 4);
       }
-      const bool on_chip = d->A_cap <= plan.AS && d->rmax <= plan.RM;
-      if (plan.NL > 0 && d->nlinks <= plan.NL) {
-        d->l_res = reinterpret_cast<double*>(take(plan.NL * 8));
-        d->l_cnt = reinterpret_cast<int*>(take(plan.NL * 4));
-        d->s_tl = reinterpret_cast<unsigned short*>(take(plan.NL * 2));
-        if (on_chip) {
-          d->c_mem = reinterpret_cast<unsigned short*>(take(plan.AS * plan.RM * 2));
-          d->c_frz = reinterpret_cast<uint8_t*>(take(plan.AS + 4));
-          d->c_mb = reinterpret_cast<unsigned short*>(take(plan.NL * 2));
-          d->c_end = reinterpret_cast<unsigned short*>(take(plan.NL * 2));
-          d->c_sat = reinterpret_cast<unsigned short*>(take(plan.NL * 2));
-        }
+      if (plan.NL > 0 && d->nlinks <= plan.NL && d->TS_cap > 0) {
+        d->l2s = reinterpret_cast<unsigned short*>(take(plan.NL * 2));
+        d->sl_res = reinterpret_cast<double*>(take(plan.TS * 8));
+        d->sl_cnt = reinterpret_cast<int*>(take(plan.TS * 4));
+        d->sl_link = reinterpret_cast<unsigned short*>(take(plan.TS * 2));
+        d->sl_mb = reinterpret_cast<unsigned short*>(take(plan.TS * 2));
+        d->sl_end = reinterpret_cast<unsigned short*>(take(plan.TS * 2));
+        d->sl_tl = reinterpret_cast<unsigned short*>(take(plan.TS * 2));
+        d->sl_sat = reinterpret_cast<unsigned short*>(take(plan.TS * 2));
+        if (d->TS_cap > plan.TS) d->TS_cap = plan.TS;
+        slots_on_chip = true;
       }
     }
+    slots_on_chip = __shfl_sync(0xffffffffu, slots_on_chip, 0);
     __syncwarp();
-    const bool on_chip = d->A_cap <= plan.AS && d->rmax <= plan.RM;
-    const bool links_on_chip = plan.NL > 0 && d->nlinks <= plan.NL;
-    if (on_chip && links_on_chip) {
-      Engine<WarpLanes, true, true> eng(*d);
+    if (slots_on_chip) {
+      Engine<WarpLanes, false, true> eng(*d);
       eng.run();
     } else {
       Engine<WarpLanes, false, false> eng(*d);
@@ -187,7 +170,7 @@ class CudaBackend final : public Backend {
     if (n) ck(cudaMemcpyAsync(h, d, n, cudaMemcpyDeviceToHost, stream_), "D2H");
   }
   void launch(const mfb::Inst* d, const int* order, int n, const LaunchHint& hint) override {
-    const mfb::SmemPlan plan = mfb::make_plan(hint.rmax, hint.nlinks);
+    const mfb::SmemPlan plan = mfb::make_plan(hint.nlinks);
     int per_sm = 0;
     ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mfb::mfsim_engine_kernel, 32,
                                                      plan.bytes),

@@ -207,13 +207,20 @@ struct Inst {
   int* s_ord;       // class order (active positions)
   int* s_cls;       // class start offsets (+1 sentinel)
   int* s_ul;        // unfrozen members of the class being filled
-  // on-chip class filling (engine allocate_chip): 16-bit link->member
-  // incidence of the class, per-link extents, saturated-link list, flags
-  unsigned short* c_mem;  // [A_cap * rmax]
-  unsigned short* c_mb;   // [nlinks] member list start
-  unsigned short* c_end;  // [nlinks] member list end / fill cursor
-  unsigned short* c_sat;  // [nlinks]
-  uint8_t* c_frz;         // [A_cap]
+  // slot filling (engine allocate_slots): the links of this step's active
+  // routes get compact slots; per-slot state is small enough for shared memory
+  int TS_cap;              // slot capacity (0: always the per-link variant)
+  unsigned short* l2s;     // [nlinks] link -> slot, 0xFFFF = none (kept so)
+  unsigned short* a_sl;    // [A_cap * rmax] slot ids of active routes (this step)
+  double* sl_res;          // [TS] residual
+  int* sl_cnt;             // [TS] unfrozen members of the class being filled
+  unsigned short* sl_link; // [TS] slot -> link
+  unsigned short* sl_mb;   // [TS] class member list start
+  unsigned short* sl_end;  // [TS] class member list end / fill cursor
+  unsigned short* sl_tl;   // [TS] live slots of the class
+  unsigned short* sl_sat;  // [TS] slots saturated this round
+  unsigned short* c_mem;   // [A_cap * rmax] slot -> member incidence
+  uint8_t* c_frz;          // [A_cap] member frozen flags
   unsigned short* s_tl;  // links touched by that class [nlinks]
   int* srt;         // sorted-subset order of the last decide (flow ids)
   int* srt_add;     // flows released since the last decide

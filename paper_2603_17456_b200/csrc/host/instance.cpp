@@ -509,9 +509,8 @@ void carve_instance(Carver& c, const InstanceInput& in, Inst& d, const Inst& top
     for (auto& cf : m->coflows) CM += static_cast<long>(cf.members.size());
     E = B * 3 + F + 64 + in.e_boost;
   }
-  A = in.a_cap > 0 ? in.a_cap : std::min<long>(std::max<long>(F, 1), kSmemActive);
-  // test knob: exercise the global-memory variant of the engine
-  if (std::getenv("MFSIM_FORCE_GLOBAL") && A <= kSmemActive) A = kSmemActive + 1;
+  A = in.a_cap > 0 ? in.a_cap : std::min<long>(std::max<long>(F, 1), kDefaultActive);
+
   A = std::max<long>(A, 1);
   const long X = A * d.rmax;
   const int LR = t.lr_cap;
@@ -678,10 +677,22 @@ void carve_instance(Carver& c, const InstanceInput& in, Inst& d, const Inst& top
   d.s_ord = c.S<int>(2 * pA);
   d.s_cls = c.S<int>(nA + 1);
   d.s_ul = c.S<int>(nA);
+  // slot filling state: host-sized for the global fallback (the kernel stages
+  // the per-slot arrays in shared memory when they fit its plan)
+  const size_t nts = std::min<size_t>(nl, nA * d.rmax);
+  d.TS_cap = (std::getenv("MFSIM_FORCE_GLOBAL") || nA * d.rmax > 65535) ? 0 : static_cast<int>(nts);
+  if (const char* cap = std::getenv("MFSIM_SLOT_CAP"))  // test knob: per-step slot overflow
+    d.TS_cap = std::min(d.TS_cap, std::atoi(cap));
+  d.l2s = c.S<unsigned short>(nl);
+  d.a_sl = c.S<unsigned short>(nA * d.rmax);
+  d.sl_res = c.S<double>(nts);
+  d.sl_cnt = c.S<int>(nts);
+  d.sl_link = c.S<unsigned short>(nts);
+  d.sl_mb = c.S<unsigned short>(nts);
+  d.sl_end = c.S<unsigned short>(nts);
+  d.sl_tl = c.S<unsigned short>(nts);
+  d.sl_sat = c.S<unsigned short>(nts);
   d.c_mem = c.S<unsigned short>(nA * d.rmax);
-  d.c_mb = c.S<unsigned short>(nl);
-  d.c_end = c.S<unsigned short>(nl);
-  d.c_sat = c.S<unsigned short>(nl);
   d.c_frz = c.S<uint8_t>(nA + 4);
   d.s_tl = c.S<unsigned short>(nl);
   d.srt = c.S<int>(nA);

@@ -23,9 +23,10 @@ namespace mfh {
 // First-attempt capacities; they match the per-warp shared-memory plan of the
 // kernel, so instances that stay within them run with their hot state on chip.
 // An instance that outgrows one is re-run with a larger, global-memory bound.
-constexpr int kSmemActive = 256;
-constexpr int kSmemEvents = 128;
-constexpr int kSmemLinks = 1024;
+constexpr int kDefaultActive = 1024;  // first-attempt active-set capacity
+constexpr int kSmemEvents = 64;       // event pool staged on chip
+constexpr int kSmemLinks = 1024;      // link -> slot map staged on chip
+constexpr int kSmemSlots = 256;       // per-slot filling state staged on chip
 
 struct LaunchHint {
   int rmax = 1;    // longest route of any instance

@@ -44,3 +44,11 @@ def test_global_memory_variant_workload(emu, name, monkeypatch):
     monkeypatch.setenv("MFSIM_FORCE_GLOBAL", "1")
     res = run_config(cases.workload_cases()[name], lib=emu)
     assert mismatches(res, "workload", name) == []
+
+
+@pytest.mark.parametrize("name", ["cluster8_400_mfs", "fattree_karuna", "sanity_sjf", "example_fs"])
+def test_slot_overflow_steps_fall_back(emu, name, monkeypatch):
+    """steps whose links exceed the slot capacity take the per-link filling"""
+    monkeypatch.setenv("MFSIM_SLOT_CAP", "6")
+    res = run_config(cases.workload_cases()[name], lib=emu)
+    assert mismatches(res, "workload", name) == []
