@@ -150,6 +150,7 @@ struct Sc {
   int n_slots;
   bool bk_slots;
   int bk_n;
+  bool rel_idx;
   int dirty;
   int err, chk;
   long long pruned;
@@ -496,6 +497,7 @@ struct Engine {
             pos = I.sl_end[sl] + popc32(peers & g.lanemask_lt());
             I.y_key[pos] = I.x_hi[e];
             I.y_val[pos] = I.x_val[e];
+            I.y_aux[pos] = I.x_aux[e];
           }
           g.sync();
           if (e < n && (peers >> g.lane()) == 1u) I.sl_end[sl] = (unsigned short)(pos + 1);
@@ -543,6 +545,7 @@ struct Engine {
         const int pos = I.l_off[l] + popc32(peers & g.lanemask_lt());
         I.y_key[pos] = I.x_hi[e];
         I.y_val[pos] = I.x_val[e];
+        I.y_aux[pos] = I.x_aux[e];
       }
       g.sync();
       if (e < n && (peers >> g.lane()) == 1u) I.l_off[l] += popc32(peers);
@@ -602,10 +605,12 @@ struct Engine {
         const int fid = I.a_fid[p];
         const unsigned long long key = ((unsigned long long)I.f_band[fid] << 16) | I.f_level[fid];
         const double r = I.a_rate[p];
+        const int hx = I.f_hidx[fid];
         for (int k = 0; k < c; ++k) {
           I.x_seg[n + off + k] = arl(p, k);
           I.x_hi[n + off + k] = key;
           I.x_val[n + off + k] = r;
+          I.x_aux[n + off + k] = hx;
         }
       }
       n += tot;
@@ -623,15 +628,18 @@ struct Engine {
       for (int a = e0 + 1; a < e1; ++a) {
         const unsigned long long k = I.y_key[a];
         const double v = I.y_val[a];
+        const int ax = I.y_aux[a];
         const unsigned long long vb = dbits(v);
         int m = a;
         while (m > e0 && (I.y_key[m - 1] > k || (I.y_key[m - 1] == k && dbits(I.y_val[m - 1]) > vb))) {
           I.y_key[m] = I.y_key[m - 1];
           I.y_val[m] = I.y_val[m - 1];
+          I.y_aux[m] = I.y_aux[m - 1];
           --m;
         }
         I.y_key[m] = k;
         I.y_val[m] = v;
+        I.y_aux[m] = ax;
       }
       double run = 0.0;
       for (int a = e0; a < e1; ++a) {
@@ -720,6 +728,38 @@ struct Engine {
     s.h_ready = 1;
   }
 
+  // load_fraction over a live LinkLoadIndex: the contributors of link l are
+  // the bucket prefix with key < (band, level); summed in unordered_map order
+  // (two or fewer: any order is exact)
+  MF_NOINLINE double load_fraction_idx(int l, int band, int level) {
+    int e0, e1;
+    double used = 0.0;
+    if (bucket_of(l, &e0, &e1)) {
+      const unsigned long long want = ((unsigned long long)band << 16) | (unsigned long long)level;
+      int lo = e0, hi = e1;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (I.y_key[mid] < want) lo = mid + 1; else hi = mid;
+      }
+      const int cnt = lo - e0;
+      if (cnt <= 2) {
+        for (int i = e0; i < lo; ++i) used = dadd(used, I.y_val[i]);
+      } else {
+        if (!s.h_ready) build_hash_order();
+        for (int i = g.lane(); i < cnt; i += G::N) {
+          I.x_hi[i] = (unsigned long long)I.h_rank[I.y_aux[e0 + i]];
+          I.x_lo[i] = 0;
+          I.x_val[i] = I.y_val[e0 + i];
+        }
+        g.sync();
+        sort_x(cnt);
+        for (int i = 0; i < cnt; ++i) used = dadd(used, I.x_val[i]);
+      }
+    }
+    const double v = ddiv(used, I.cap[l]);
+    return v < 0.0 ? 0.0 : (1.0 < v ? 1.0 : v);
+  }
+
   // load_fraction (allocator.cpp:128-141): sum in unordered_map order
   MF_NOINLINE double load_fraction(int l, int band, int level) {
     int cnt = 0;
@@ -791,7 +831,8 @@ struct Engine {
       double best_eff = MF_INF;
       for (int k = 0; k < rn; ++k) {
         int l = I.route_links[rb + k];
-        double rho = use_idx ? index_fraction(l, pb, pl) : load_fraction(l, pb, pl);
+        double rho = use_idx ? index_fraction(l, pb, pl)
+                             : (s.rel_idx ? load_fraction_idx(l, pb, pl) : load_fraction(l, pb, pl));
         double eff = dmul(I.cap[l], dsub(1.0, rho));
         if (eff < best_eff) best_eff = eff;
       }
@@ -1264,6 +1305,7 @@ struct Engine {
           I.x_seg[n + off + k] = arl(p, k);
           I.x_hi[n + off + k] = 0;
           I.x_val[n + off + k] = want;
+          I.x_aux[n + off + k] = 0;
         }
         I.s_cap[p] = want;  // stash: capped below
       }
@@ -2086,10 +2128,24 @@ struct Engine {
       }
     }
     const int po = I.pl_poff[idx], pc = I.pl_pcnt[idx];
+    // MFS initial P2D priorities query the last allocation per route link; in
+    // workload mode no release in this loop can finish a flow (sizes > 0,
+    // distinct hosts), so one index built after the promotion review serves
+    // every release of the layer
+    int nxr = 0;
+    if (I.p.policy == POL_MFS && I.p.workload_mode && pc > 0) {
+      nxr = build_index();
+      if (s.err) return;
+      s.rel_idx = true;
+    }
     for (int k = 0; k < pc; ++k) {
       int fid = I.ppool[po + k];
       if (!(I.f_scripted[fid] & 1) && I.f_state[fid] == FL_PENDING) release_flow(fid);
       if (s.err) return;
+    }
+    if (s.rel_idx) {
+      s.rel_idx = false;
+      bucket_release(nxr);
     }
     try_start_layers(b);
     check_pipeline_done(b);
@@ -2783,6 +2839,7 @@ struct Engine {
     s.n_srt = 0;
     s.n_add = 0;
     s.n_slots = 0;
+    s.rel_idx = false;
     for (int l = g.lane(); l < I.nlinks; l += G::N) I.l2s[l] = 0xFFFFu;
     if (!I.host_init) {
       init_state();

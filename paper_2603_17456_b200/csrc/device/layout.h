@@ -239,6 +239,8 @@ struct Inst {
   int* x_seg;       // segment heads / entry link ids
   unsigned long long* y_key;  // entries bucketed by link (stable)
   double* y_val;
+  int* x_aux;       // per-entry payload (allocation insertion index)
+  int* y_aux;
   // ---- Algorithm 1 scratch
   int* g_batches;   // live (undrained) batch list [B_cap]
   int* g_req;       // in-flight unpruned requests [n_req]

@@ -713,6 +713,8 @@ void carve_instance(Carver& c, const InstanceInput& in, Inst& d, const Inst& top
   d.x_seg = c.S<int>(pX);
   d.y_key = c.S<unsigned long long>(pX);
   d.y_val = c.S<double>(pX);
+  d.x_aux = c.S<int>(pX);
+  d.y_aux = c.S<int>(pX);
   const size_t pB = static_cast<size_t>(pow2(static_cast<long>(nB)));
   d.g_batches = c.S<int>(nB);
   d.g_req = c.S<int>(nr);
