@@ -103,32 +103,34 @@ class RefError(RuntimeError):
         self.code = code
 
 
-_lib = None
+_libs = {}
 
 
-def lib():
-    global _lib
-    if _lib is None:
-        if not os.path.exists(REF_SO):
-            raise FileNotFoundError(f"{REF_SO} missing: run `make -C oracle` where /root/reference exists")
-        _lib = C.CDLL(REF_SO)
+def lib(so: str = REF_SO):
+    """the reference library (default) or the C restatement (ORACLE_SO)"""
+    if so not in _libs:
+        if not os.path.exists(so):
+            raise FileNotFoundError(f"{so} missing: run `make -C oracle`")
+        L = C.CDLL(so)
         for fn in ("ref_run_config", "ref_run_manual", "ref_derive_deadlines"):
-            getattr(_lib, fn).argtypes = [C.c_char_p, C.POINTER(C.POINTER(_RefResult))]
-            getattr(_lib, fn).restype = C.c_int
-        _lib.ref_free.argtypes = [C.POINTER(_RefResult)]
-        _lib.ref_allocate_star.restype = C.c_int
-    return _lib
+            getattr(L, fn).argtypes = [C.c_char_p, C.POINTER(C.POINTER(_RefResult))]
+            getattr(L, fn).restype = C.c_int
+        L.ref_free.argtypes = [C.POINTER(_RefResult)]
+        if hasattr(L, "ref_allocate_star"):
+            L.ref_allocate_star.restype = C.c_int
+        _libs[so] = L
+    return _libs[so]
 
 
-def available() -> bool:
-    return os.path.exists(REF_SO)
+def available(so: str = REF_SO) -> bool:
+    return os.path.exists(so)
 
 
-def _convert(p) -> SimResult:
+def _convert(p, so=REF_SO) -> SimResult:
     r = p.contents
     if r.err:
         code, msg = r.err, r.errmsg.decode()
-        lib().ref_free(p)
+        lib(so).ref_free(p)
         raise RefError(code, msg)
     out = SimResult(
         events=r.events,
@@ -153,26 +155,26 @@ def _convert(p) -> SimResult:
         t_run_s=r.t_run_s,
         t_setup_s=r.t_setup_s,
     )
-    lib().ref_free(p)
+    lib(so).ref_free(p)
     return out
 
 
-def run_config(text: str) -> SimResult:
+def run_config(text: str, so: str = REF_SO) -> SimResult:
     p = C.POINTER(_RefResult)()
-    lib().ref_run_config(text.encode(), C.byref(p))
-    return _convert(p)
+    lib(so).ref_run_config(text.encode(), C.byref(p))
+    return _convert(p, so)
 
 
-def run_manual(spec: str) -> SimResult:
+def run_manual(spec: str, so: str = REF_SO) -> SimResult:
     p = C.POINTER(_RefResult)()
-    lib().ref_run_manual(spec.encode(), C.byref(p))
-    return _convert(p)
+    lib(so).ref_run_manual(spec.encode(), C.byref(p))
+    return _convert(p, so)
 
 
-def derive_deadlines(text: str):
+def derive_deadlines(text: str, so: str = REF_SO):
     p = C.POINTER(_RefResult)()
-    lib().ref_derive_deadlines(text.encode(), C.byref(p))
-    r = _convert(p)
+    lib(so).ref_derive_deadlines(text.encode(), C.byref(p))
+    r = _convert(p, so)
     return r.req_arrival, r.req_deadline
 
 
