@@ -3,10 +3,12 @@
 
 Workload (BASELINE.json configs[3]): the batched sweep on the ft128 fabric
 ("1024 GPUs" = 128 hosts x 8 NICs, k=8 fat-tree), 2000 requests per instance,
-cells = offered load x SLO multiplier x seed x policy. A step = one device
-launch that simulates S full instances of that grid from their initial state
-on each rank (weak scaling: S fixed per GPU; ranks take disjoint cells; no
-collective on the data path). flow-events = RunResult::events
+cells = offered load x SLO multiplier x seed x policy. S full-size instances
+of that grid are resident per rank (weak scaling: S fixed per GPU; ranks take
+disjoint cells; no collective on the data path). A step = one device launch
+that advances every instance by `--budget` events (instances suspend to HBM
+and resume exactly), so every step is steady-state work over the whole mix;
+the warm-up launches start the instances. flow-events = RunResult::events
 (engine.cpp:611), summed over instances.
 
   value : events / device time of the timed launches (inputs resident in HBM,
@@ -41,7 +43,9 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--instances", type=int, default=int(os.environ.get("MFSIM_BENCH_INSTANCES", 1184)),
-                    help="instances per rank per step")
+                    help="resident instances per rank")
+    ap.add_argument("--budget", type=int, default=20000,
+                    help="events each instance advances per step (launch)")
     ap.add_argument("--requests", type=int, default=2000, help="requests per instance (configs[3]: 2000)")
     ap.add_argument("--cpu-sample-s", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -194,7 +198,8 @@ def workload_config(args):
         "workload": "configs[3] sweep: ft128 fat-tree (128 hosts x 8 NICs, k=8, 768 links), "
                     "16 units x 4 hosts + 64 decode, cells = load {0.3..0.9} x SLO {1..5} x "
                     "seed {1..64} x policy {fs,sjf,edf,karuna,mfs}",
-        "instances_per_rank_per_step": args.instances,
+        "instances_per_rank": args.instances,
+        "events_per_instance_per_step": args.budget,
         "requests_per_instance": args.requests,
         "l2": "inputs larger than L2 (per-step working set >> 126 MB)",
         "parallelism": f"instance-sharded x{args.gpus}",
@@ -205,8 +210,6 @@ def main():
     args = parse()
     rank, world, local = dist_env()
     if args.impl == "reference":
-        if world > 1:
-            import torch.distributed as dist  # noqa: F401
         reference_arm(args, rank, world)
         return
 
@@ -227,16 +230,15 @@ def main():
     batch = DeviceBatch(local, lib, stream=stream.cuda_stream)
     for c in cells:
         batch.add_config(sweep.sweep_config(c, requests=args.requests, lib=lib))
-    batch.prepare()
+    batch.prepare()  # workload synthesis + batched derive_slos (device)
+    batch.upload()   # inputs resident in HBM; instances at their initial state
     setup_s = time.perf_counter() - t0
-    # first full run: capacity retries settle here (not timed), results kept for checks
-    batch.run(0)
-    for i in range(len(batch)):
-        batch.raise_for_status(i)
-    events_per_step = sum(batch.stats(i).events for i in range(len(batch)))
-    algo_bytes = sum(batch.stats(i).algo_bytes for i in range(len(batch)))
-    met = sum(batch.stats(i).slo_met for i in range(len(batch)))
-    reqs = sum(batch.stats(i).requests for i in range(len(batch)))
+    n = len(batch)
+
+    def progress():
+        batch.download(0)
+        return (sum(batch.stats(i).events for i in range(n)),
+                sum(batch.stats(i).algo_bytes for i in range(n)))
 
     def barrier():
         torch.cuda.synchronize()
@@ -244,41 +246,48 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
+    # warm-up: the first budgeted launches start every instance
     for _ in range(args.warmup):
-        batch.launch()
+        batch.launch_budget(args.budget)
     barrier()
+    ev0, by0 = progress()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
     with Clocks(local) as clk:
         start.record(stream)
         for _ in range(args.steps):
-            batch.launch()
+            batch.launch_budget(args.budget)
         end.record(stream)
         barrier()
     dev_ms = start.elapsed_time(end)
-    # e2e through the C ABI with host buffers (H2D + launch + D2H each step)
+    ev1, by1 = progress()
+    events, algo_bytes = ev1 - ev0, by1 - by0
+    # e2e through the C ABI: H2D of the inputs, launch, D2H of per-request results
     barrier()
     e0 = time.perf_counter()
     for _ in range(args.steps):
-        batch.upload()
-        batch.launch()
+        batch.upload_inputs()
+        batch.launch_budget(args.budget)
         batch.download(0)
     barrier()
     e2e_s = time.perf_counter() - e0
+    ev2, _ = progress()
+    e2e_events = ev2 - ev1
     h2d, d2h = batch.h2d_bytes, batch.d2h_bytes
 
-    t = torch.tensor([dev_ms, e2e_s, float(events_per_step)], dtype=torch.float64, device="cuda")
+    t = torch.tensor([dev_ms, e2e_s, float(events), float(e2e_events), float(algo_bytes)],
+                     dtype=torch.float64, device="cuda")
     if world > 1:
         mx = t.clone()
         dist.all_reduce(mx, op=dist.ReduceOp.MAX)
         sm = t.clone()
         dist.all_reduce(sm, op=dist.ReduceOp.SUM)
-        dev_ms, e2e_s, total_events = mx[0].item(), mx[1].item(), sm[2].item()
-    else:
-        total_events = float(events_per_step)
-    value = total_events * args.steps / (dev_ms / 1000.0)
-    e2e = total_events * args.steps / e2e_s
+        dev_ms, e2e_s = mx[0].item(), mx[1].item()
+        events, e2e_events = sm[2].item(), sm[3].item()
+    value = events / (dev_ms / 1000.0)
+    e2e = e2e_events / e2e_s
     kernel_ms = dev_ms / args.steps
-    achieved = algo_bytes / (kernel_ms / 1000.0) / 1e9
+    achieved = algo_bytes / (dev_ms / 1000.0) / 1e9  # rank 0's launches
     try:
         peaks = json.load(open(PEAKS))
         peak, peak_src = float(peaks["hbm_gbs"]), "measured"
@@ -299,8 +308,7 @@ def main():
                          "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
                          "kernel": "mfsim_engine_kernel"},
             "clocks": clk.summary(),
-            "events_per_step_rank0": events_per_step,
-            "slo_attainment_rank0": met / max(reqs, 1),
+            "events_per_step": events / args.steps,
             "setup_s_rank0": setup_s,
             "device_bytes_rank0": batch.device_bytes,
         }
@@ -312,8 +320,8 @@ def main():
                 line["cpu_baseline"] = {
                     "value": r["events"] / r["wall_s"], "unit": "events/s", "cores": r["cores"],
                     "kind": "reference",
-                    "sample": f"{r['instances']} sweep instances ({args.requests} requests each) "
-                              f"in {r['wall_s']:.1f}s on {r['cores']} host threads"}
+                    "sample": f"{r['instances']} sweep instances ({args.requests} requests each, run to "
+                              f"completion) in {r['wall_s']:.1f}s on {r['cores']} host threads"}
             except Exception as e:  # the oracle library is absent: report why
                 line["cpu_baseline"] = {"value": None, "unit": "events/s", "cores": 0,
                                         "kind": "reference", "sample": f"unavailable: {e}"}

@@ -67,8 +67,18 @@ int mfsim_dev_add_manual(mfsim_dev* d, const char* spec);
 int mfsim_dev_prepare(mfsim_dev* d);
 /* H2D of all packed inputs (stream-ordered) */
 int mfsim_dev_upload(mfsim_dev* d);
-/* launch the device event loops on the stream; returns immediately */
+/* every instance from its initial state to completion, one launch on the
+ * stream; returns immediately */
 int mfsim_dev_launch(mfsim_dev* d);
+/* H2D of the packed inputs only (running instances are not reset) */
+int mfsim_dev_upload_inputs(mfsim_dev* d);
+/* back to the initial state without launching */
+int mfsim_dev_reset(mfsim_dev* d);
+/* advance every unfinished instance by at most `budget` events (suspended
+ * instances resume exactly where they stopped); returns immediately */
+int mfsim_dev_launch_budget(mfsim_dev* d, long long budget);
+/* instances not finished yet (synchronises the stream) */
+int mfsim_dev_remaining(mfsim_dev* d);
 /* wait for the stream; *kernel_ms receives the last launch's device time */
 int mfsim_dev_sync(mfsim_dev* d, double* kernel_ms);
 /* D2H: detail 0 = per-request results, 1 = + coflows, 2 = + flows/batches */

@@ -196,7 +196,35 @@ int mfsim_dev_upload(mfsim_dev* d) {
 
 int mfsim_dev_launch(mfsim_dev* d) {
   if (!d || !d->batch) return fail(MFSIM_ERR_INVALID_ARG, "mfsim_dev_launch: nothing prepared");
-  return guarded([&] { d->batch->launch(); });
+  return guarded([&] {
+    d->batch->reset();
+    d->batch->launch(0);
+  });
+}
+
+int mfsim_dev_upload_inputs(mfsim_dev* d) {
+  if (!d || !d->batch) return fail(MFSIM_ERR_INVALID_ARG, "mfsim_dev_upload_inputs: nothing prepared");
+  return guarded([&] {
+    d->batch->upload_inputs();
+    d->h2d = static_cast<long long>(d->batch->input_bytes());
+  });
+}
+
+int mfsim_dev_reset(mfsim_dev* d) {
+  if (!d || !d->batch) return fail(MFSIM_ERR_INVALID_ARG, "mfsim_dev_reset: nothing prepared");
+  return guarded([&] { d->batch->reset(); });
+}
+
+int mfsim_dev_launch_budget(mfsim_dev* d, long long budget) {
+  if (!d || !d->batch) return fail(MFSIM_ERR_INVALID_ARG, "mfsim_dev_launch_budget: nothing prepared");
+  return guarded([&] { d->batch->launch(budget); });
+}
+
+int mfsim_dev_remaining(mfsim_dev* d) {
+  if (!d || !d->batch) return -1;
+  int r = -1;
+  guarded([&] { r = d->batch->remaining(); });
+  return r;
 }
 
 int mfsim_dev_sync(mfsim_dev* d, double* kernel_ms) {

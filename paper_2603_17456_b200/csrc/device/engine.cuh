@@ -2809,7 +2809,7 @@ struct Engine {
     g.sync();
   }
 
-  MF_NOINLINE void run() {
+  MF_NOINLINE void start() {
     const long long seq0 = I.seq0;
     const int n_ev0 = I.n_ev0, n_flows0 = I.n_flows0, n_batches0 = I.n_batches0,
               n_coflows0 = I.n_coflows0;
@@ -2840,7 +2840,9 @@ struct Engine {
     s.n_add = 0;
     s.n_slots = 0;
     s.rel_idx = false;
+    for (int k = 0; k < 32; ++k) s.cy[k] = 0;
     for (int l = g.lane(); l < I.nlinks; l += G::N) I.l2s[l] = 0xFFFFu;
+    pool_copy(true, n_ev0);  // host-prepared initial events (manual mode)
     if (!I.host_init) {
       init_state();
     } else {
@@ -2855,13 +2857,57 @@ struct Engine {
     }
     recompute_rates();
     s.dirty = 0;
-    for (int k = 0; k < 32; ++k) s.cy[k] = 0;
+  }
+
+  // pool entries between the on-chip pool and its global home
+  MF_FN void pool_copy(bool to_chip, int n) {
+    if (!I.e_t_home) return;
+    for (int i = g.lane(); i < n; i += G::N) {
+      if (to_chip) {
+        I.e_t[i] = I.e_t_home[i];
+        I.e_seq[i] = I.e_seq_home[i];
+        I.e_kind[i] = I.e_kind_home[i];
+        I.e_a[i] = I.e_a_home[i];
+        I.e_b[i] = I.e_b_home[i];
+      } else {
+        I.e_t_home[i] = I.e_t[i];
+        I.e_seq_home[i] = I.e_seq[i];
+        I.e_kind_home[i] = I.e_kind[i];
+        I.e_a_home[i] = I.e_a[i];
+        I.e_b_home[i] = I.e_b[i];
+      }
+    }
+    g.sync();
+  }
+
+  // Runs the instance's event loop for at most `budget` events (<= 0: to the
+  // end). A suspended instance keeps all state in HBM plus its scalar state in
+  // sc_blob and resumes exactly where it stopped. Returns true when finished.
+  MF_NOINLINE bool run(long long budget) {
+    static_assert(sizeof(Sc) <= kScBlob, "scalar state exceeds its blob");
+    const int ph = *I.phase;
+    if (ph == 2) return false;
+    if (ph == 1) {  // resume
+      const unsigned int* src = reinterpret_cast<const unsigned int*>(I.sc_blob);
+      unsigned int* dst = reinterpret_cast<unsigned int*>(&s);
+      for (int w = 0; w < (int)(sizeof(Sc) / 4); ++w) dst[w] = src[w];
+      for (int l = g.lane(); l < I.nlinks; l += G::N) I.l2s[l] = 0xFFFFu;
+      g.sync();
+      pool_copy(true, s.n_ev);
+    } else {
+      start();
+    }
+    const long long stop_at = budget > 0 ? s.events + budget : 0x7fffffffffffffffLL;
+    bool finished = false;
     while (!s.err) {
+      if (s.events >= stop_at) break;
       MF_TIC(tn);
       Ev e = next_event();
       MF_TOC(OUT_CY_NEXT, tn);
-      if (e.src == 0) break;
-      if (e.t > s.horizon) break;
+      if (e.src == 0 || e.t > s.horizon) {
+        finished = true;
+        break;
+      }
       int kind, a, b;
       if (e.src == 1) {
         kind = EV_ARRIVAL;
@@ -2951,6 +2997,21 @@ struct Engine {
         s.dirty = 0;
       }
     }
+    if (s.err) finished = true;
+    if (!finished) {  // suspend: scalar state and pool to HBM
+      g.sync();
+      if (g.leader()) {
+        const unsigned int* src = reinterpret_cast<const unsigned int*>(&s);
+        unsigned int* dst = reinterpret_cast<unsigned int*>(I.sc_blob);
+        for (int w = 0; w < (int)(sizeof(Sc) / 4); ++w) dst[w] = src[w];
+        *I.phase = 1;
+        I.out[OUT_EVENTS] = s.events;  // progress, visible while suspended
+        I.out[OUT_STEPS] = s.steps;
+        I.out[OUT_ALGO_BYTES] = s.algo_bytes;
+      }
+      pool_copy(false, s.n_ev);
+      return false;
+    }
     if (!s.err) finalize();
     if (g.leader()) {
       I.out[OUT_STATUS] = s.err;
@@ -2970,8 +3031,10 @@ struct Engine {
       I.out[OUT_MAXTOUCH] = s.max_touch;
       I.out[OUT_MAXPOOL] = s.max_pool;
       for (int k = 0; k < 32; ++k) I.out[OUT_CY_NEXT + k] = s.cy[k];
+      *I.phase = 2;
     }
     g.sync();
+    return true;
   }
 
   // engine.cpp:659-707: per-coflow stall and per-batch stall (coflow id order)

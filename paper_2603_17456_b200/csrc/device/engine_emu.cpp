@@ -28,14 +28,16 @@ class EmuBackend final : public Backend {
   void d2h(void* h, const void* d, size_t n) override {
     if (n) std::memcpy(h, d, n);
   }
-  void launch(const mfb::Inst* d, const int*, int n, const LaunchHint&) override {
+  void launch(const mfb::Inst* d, const int*, int n, const LaunchHint&, long long budget) override {
     for (int i = 0; i < n; ++i) {
       mfb::Inst local = d[i];
       mfb::Engine<mfb::SerialLanes, false, false> eng(local);
-      eng.run();
+      if (eng.run(budget)) --remaining_;
     }
     ++launches_;
   }
+  void set_remaining(int n) override { remaining_ = n; }
+  int remaining() override { return remaining_; }
   void sync() override {}
   void set_stream(void*) override {}
   double last_kernel_ms() const override { return 0.0; }
@@ -43,6 +45,7 @@ class EmuBackend final : public Backend {
 
  private:
   int launches_ = 0;
+  int remaining_ = 0;
 };
 
 }  // namespace

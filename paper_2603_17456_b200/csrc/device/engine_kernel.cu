@@ -47,7 +47,8 @@ __host__ inline SmemPlan make_plan(int nlinks) {
 
 __global__ void __launch_bounds__(32)
     mfsim_engine_kernel(const Inst* __restrict__ insts, const int* __restrict__ order, int n,
-                        int* __restrict__ next, SmemPlan plan) {
+                        int* __restrict__ next, SmemPlan plan, long long budget,
+                        int* __restrict__ remaining) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31;
   Inst* d = reinterpret_cast<Inst*>(smem);
@@ -77,13 +78,11 @@ __global__ void __launch_bounds__(32)
         int* ek = reinterpret_cast<int*>(take(plan.ES * 4));
         int* ea = reinterpret_cast<int*>(take(plan.ES * 4));
         int* eb = reinterpret_cast<int*>(take(plan.ES * 4));
-        for (int e = 0; e < d->n_ev0; ++e) {  // host-prepared initial events
-          et[e] = d->e_t[e];
-          es[e] = d->e_seq[e];
-          ek[e] = d->e_kind[e];
-          ea[e] = d->e_a[e];
-          eb[e] = d->e_b[e];
-        }
+        d->e_t_home = d->e_t;  // the engine moves entries between chip and home
+        d->e_seq_home = d->e_seq;
+        d->e_kind_home = d->e_kind;
+        d->e_a_home = d->e_a;
+        d->e_b_home = d->e_b;
         d->e_t = et;
         d->e_seq = es;
         d->e_kind = ek;
@@ -107,13 +106,15 @@ __global__ void __launch_bounds__(32)
     }
     slots_on_chip = __shfl_sync(0xffffffffu, slots_on_chip, 0);
     __syncwarp();
+    bool done;
     if (slots_on_chip) {
       Engine<WarpLanes, false, true> eng(*d);
-      eng.run();
+      done = eng.run(budget);
     } else {
       Engine<WarpLanes, false, false> eng(*d);
-      eng.run();
+      done = eng.run(budget);
     }
+    if (done && lane == 0) atomicSub(remaining, 1);
     __syncwarp();
   }
 }
@@ -136,7 +137,8 @@ class CudaBackend final : public Backend {
     stream_ = own_;
     ck(cudaEventCreate(&e0_), "cudaEventCreate");
     ck(cudaEventCreate(&e1_), "cudaEventCreate");
-    ck(cudaMalloc(&counter_, sizeof(int)), "cudaMalloc counter");
+    ck(cudaMalloc(&counter_, 2 * sizeof(int)), "cudaMalloc counter");
+    ck(cudaMallocHost(&remain_host_, sizeof(int)), "cudaMallocHost");
     ck(cudaDeviceGetAttribute(&sms_, cudaDevAttrMultiProcessorCount, device), "attr");
     ck(cudaFuncSetAttribute(mfb::mfsim_engine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             200 * 1024),
@@ -146,6 +148,7 @@ class CudaBackend final : public Backend {
   }
   ~CudaBackend() override {
     cudaFree(counter_);
+    cudaFreeHost(remain_host_);
     cudaEventDestroy(e0_);
     cudaEventDestroy(e1_);
     cudaStreamDestroy(own_);
@@ -169,7 +172,8 @@ class CudaBackend final : public Backend {
   void d2h(void* h, const void* d, size_t n) override {
     if (n) ck(cudaMemcpyAsync(h, d, n, cudaMemcpyDeviceToHost, stream_), "D2H");
   }
-  void launch(const mfb::Inst* d, const int* order, int n, const LaunchHint& hint) override {
+  void launch(const mfb::Inst* d, const int* order, int n, const LaunchHint& hint,
+              long long budget) override {
     const mfb::SmemPlan plan = mfb::make_plan(hint.nlinks);
     int per_sm = 0;
     ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mfb::mfsim_engine_kernel, 32,
@@ -180,12 +184,26 @@ class CudaBackend final : public Backend {
     if (n < grid) grid = n > 0 ? n : 1;
     ck(cudaMemsetAsync(counter_, 0, sizeof(int), stream_), "memset");
     ck(cudaEventRecord(e0_, stream_), "event");
-    mfb::mfsim_engine_kernel<<<grid, 32, plan.bytes, stream_>>>(d, order, n, counter_, plan);
+    mfb::mfsim_engine_kernel<<<grid, 32, plan.bytes, stream_>>>(d, order, n, counter_, plan,
+                                                                budget, counter_ + 1);
     ck(cudaGetLastError(), "launch");
     ck(cudaEventRecord(e1_, stream_), "event");
     ++launches_;
     timed_ = true;
     last_grid_ = grid;
+  }
+  // instances not yet finished (a fresh batch sets it to n)
+  void set_remaining(int n) override {
+    *remain_host_ = n;
+    ck(cudaMemcpyAsync(counter_ + 1, remain_host_, sizeof(int), cudaMemcpyHostToDevice, stream_),
+       "remaining");
+    ck(cudaStreamSynchronize(stream_), "remaining");
+  }
+  int remaining() override {
+    ck(cudaMemcpyAsync(remain_host_, counter_ + 1, sizeof(int), cudaMemcpyDeviceToHost, stream_),
+       "remaining");
+    ck(cudaStreamSynchronize(stream_), "remaining");
+    return *remain_host_;
   }
   void sync() override {
     ck(cudaStreamSynchronize(stream_), "kernel");
@@ -205,6 +223,7 @@ class CudaBackend final : public Backend {
   cudaStream_t own_ = nullptr, stream_ = nullptr;
   cudaEvent_t e0_ = nullptr, e1_ = nullptr;
   int* counter_ = nullptr;
+  int* remain_host_ = nullptr;
   int sms_ = 148;
   int last_grid_ = 0;
   int launches_ = 0;

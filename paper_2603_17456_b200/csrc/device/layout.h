@@ -71,6 +71,7 @@ enum : int {
 };
 
 constexpr int kMaxK = 32;  // mfs.K upper bound on the device
+constexpr int kScBlob = 1024;  // bytes reserved for the suspended scalar state
 
 struct InstParams {
   int policy;
@@ -270,6 +271,14 @@ struct Inst {
   double* r_stall;  // [n_req] per-request stall = its batch's stall
   uint8_t* o_pruned;  // [n_req] output copies of r_pruned / r_batch
   int* o_rbatch;
+  // ---- suspend / resume across launches
+  int* phase;                 // 0 fresh, 1 suspended, 2 done
+  unsigned char* sc_blob;     // [kScBlob] scalar engine state while suspended
+  double* e_t_home;           // global homes of an on-chip event pool (null if
+  unsigned long long* e_seq_home;  //   the pool stayed in global memory)
+  int* e_kind_home;
+  int* e_a_home;
+  int* e_b_home;
   // ---- outputs / scalars
   long long* out;  // [OUT_N]
 };

@@ -741,6 +741,7 @@ void carve_instance(Carver& c, const InstanceInput& in, Inst& d, const Inst& top
   d.b_stall = c.S<double>(nB);
   d.r_stall = c.O<double>(nr, o_stall);
   d.out = c.O<long long>(OUT_N, o_out);
+  d.sc_blob = c.S<unsigned char>(kScBlob);
   d.o_pruned = c.O<uint8_t>(nr, o_pruned);
   d.o_rbatch = c.O<int>(nr, o_rbatch);
 
@@ -846,9 +847,11 @@ void Batch::release() {
   if (out_dev_) be_.dev_free(out_dev_);
   if (desc_dev_) be_.dev_free(desc_dev_);
   if (order_dev_) be_.dev_free(order_dev_);
+  if (phase_dev_) be_.dev_free(phase_dev_);
   in_host_ = out_host_ = in_dev_ = st_dev_ = out_dev_ = nullptr;
   desc_dev_ = nullptr;
   order_dev_ = nullptr;
+  phase_dev_ = nullptr;
 }
 
 void Batch::pack() {
@@ -896,8 +899,10 @@ void Batch::pack() {
       out_dev_ = static_cast<char*>(be_.dev_alloc(out_bytes_ + 64));
       desc_dev_ = static_cast<Inst*>(be_.dev_alloc(sizeof(Inst) * std::max(n, 1)));
       order_dev_ = static_cast<int*>(be_.dev_alloc(sizeof(int) * std::max(n, 1)));
+      phase_dev_ = static_cast<int*>(be_.dev_alloc(sizeof(int) * std::max(n, 1)));
     }
   }
+  for (int i = 0; i < n; ++i) desc_[i].phase = phase_dev_ + i;
   // claim order: estimated work descending (Karuna's capped filling and MFS's
   // promotions cost the most per event), so the longest instances start first
   std::vector<double> cost(n);
@@ -912,13 +917,24 @@ void Batch::pack() {
   std::stable_sort(order_.begin(), order_.end(), [&](int a, int b) { return cost[a] > cost[b]; });
 }
 
+void Batch::upload_inputs() { be_.h2d(in_dev_, in_host_, in_bytes_); }
+
 void Batch::upload() {
   be_.h2d(in_dev_, in_host_, in_bytes_);
   be_.h2d(desc_dev_, desc_.data(), sizeof(Inst) * desc_.size());
   be_.h2d(order_dev_, order_.data(), sizeof(int) * order_.size());
+  reset();
 }
 
-void Batch::launch() { be_.launch(desc_dev_, order_dev_, size(), hint_); }
+void Batch::reset() {
+  std::vector<int> zero(size(), 0);
+  be_.h2d(phase_dev_, zero.data(), sizeof(int) * zero.size());
+  be_.set_remaining(size());
+}
+
+void Batch::launch(long long budget) { be_.launch(desc_dev_, order_dev_, size(), hint_, budget); }
+
+int Batch::remaining() { return be_.remaining(); }
 
 size_t Batch::output_bytes(int detail) const {
   size_t b = out_bytes_;
@@ -987,7 +1003,8 @@ void Batch::run(int detail) {
   // the final capacities (a later launch() re-simulates the same batch).
   for (int attempt = 0; attempt < 16; ++attempt) {
     upload();
-    launch();
+    do launch(0);
+    while (remaining() > 0);
     download(detail);
     bool again = false;
     for (int i = 0; i < size(); ++i) {

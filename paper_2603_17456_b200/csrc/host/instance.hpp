@@ -44,8 +44,12 @@ class Backend {
   virtual void host_free(void* p) = 0;
   virtual void h2d(void* dst, const void* src, size_t n) = 0;  // stream-ordered
   virtual void d2h(void* dst, const void* src, size_t n) = 0;
-  // order: device array, a permutation of [0, n) giving the claim order
-  virtual void launch(const mfb::Inst* d_insts, const int* order, int n, const LaunchHint& hint) = 0;
+  // order: device array, a permutation of [0, n) giving the claim order;
+  // budget: events per instance in this launch (<= 0: run to completion)
+  virtual void launch(const mfb::Inst* d_insts, const int* order, int n, const LaunchHint& hint,
+                      long long budget) = 0;
+  virtual void set_remaining(int n) = 0;
+  virtual int remaining() = 0;
   virtual void sync() = 0;
   virtual void set_stream(void* stream) = 0;
   virtual double last_kernel_ms() const = 0;
@@ -114,8 +118,11 @@ class Batch {
   Batch(const Batch&) = delete;
   Batch& operator=(const Batch&) = delete;
 
-  void upload();          // H2D of all inputs (stream-ordered)
-  void launch();          // device event loops (stream-ordered)
+  void upload();          // H2D of all inputs (stream-ordered) + reset()
+  void upload_inputs();   // H2D of the inputs only (state untouched)
+  void reset();           // every instance back to its initial state (fresh run)
+  void launch(long long budget = 0);  // device event loops (stream-ordered)
+  int remaining();        // instances not finished yet (synchronises)
   void download(int detail);  // D2H; detail 0 requests, 1 +coflows, 2 +flows/batches
   // upload + launch + download, re-running instances that hit a capacity
   // bound with doubled capacities
@@ -142,6 +149,7 @@ class Batch {
   char* out_dev_ = nullptr;
   mfb::Inst* desc_dev_ = nullptr;
   int* order_dev_ = nullptr;
+  int* phase_dev_ = nullptr;
   std::vector<int> order_;
   LaunchHint hint_;
   size_t in_bytes_ = 0, st_bytes_ = 0, out_bytes_ = 0;

@@ -112,6 +112,8 @@ class Native:
             "mfsim_dev_write_report": ([vp, i, cp], i),
             "mfsim_route": ([vp, i, i, vp, vp, i, C.POINTER(i)], i),
             "mfsim_dev_counters": ([vp, i, vp, i], i),
+            "mfsim_dev_reset": ([vp], i), "mfsim_dev_upload_inputs": ([vp], i), "mfsim_dev_launch_budget": ([vp, ll], i),
+            "mfsim_dev_remaining": ([vp], i),
             "mfsim_link_count": ([vp, C.POINTER(i)], i),
         }
         for name, (args, res) in sig.items():
@@ -212,6 +214,18 @@ class DeviceBatch:
 
     def launch(self):
         self.n.check(self.n.lib.mfsim_dev_launch(self.h))
+
+    def upload_inputs(self):
+        self.n.check(self.n.lib.mfsim_dev_upload_inputs(self.h))
+
+    def reset(self):
+        self.n.check(self.n.lib.mfsim_dev_reset(self.h))
+
+    def launch_budget(self, budget: int):
+        self.n.check(self.n.lib.mfsim_dev_launch_budget(self.h, budget))
+
+    def remaining(self) -> int:
+        return self.n.lib.mfsim_dev_remaining(self.h)
 
     def sync(self) -> float:
         ms = C.c_double(0.0)

@@ -52,3 +52,21 @@ def test_slot_overflow_steps_fall_back(emu, name, monkeypatch):
     monkeypatch.setenv("MFSIM_SLOT_CAP", "6")
     res = run_config(cases.workload_cases()[name], lib=emu)
     assert mismatches(res, "workload", name) == []
+
+
+@pytest.mark.parametrize("name", ["cluster8_400_mfs", "cluster8_400_karuna", "fattree_edf", "c9_mfs"])
+def test_suspend_resume_is_exact(emu, name):
+    """event-budgeted launches (suspend / resume through HBM) change nothing"""
+    from paper_2603_17456_b200.native import DeviceBatch
+    b = DeviceBatch(0, emu)
+    b.add_config(cases.workload_cases()[name])
+    b.prepare()
+    b.upload()
+    b.reset()
+    launches = 0
+    while b.remaining() > 0:
+        b.launch_budget(61)
+        launches += 1
+    b.download(2)
+    assert launches > 2
+    assert mismatches(b.result(0, 2, reports=True), "workload", name) == []
