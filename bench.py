@@ -6,9 +6,10 @@ Workload (BASELINE.json configs[3]): the batched sweep on the ft128 fabric
 cells = offered load x SLO multiplier x seed x policy. S full-size instances
 of that grid are resident per rank (weak scaling: S fixed per GPU; ranks take
 disjoint cells; no collective on the data path). A step = one device launch
-that advances every instance by `--budget` events (instances suspend to HBM
-and resume exactly), so every step is steady-state work over the whole mix;
-the warm-up launches start the instances. flow-events = RunResult::events
+in which every warp advances its instance for `--slice-ms` of device time and
+then suspends it to HBM (resumed exactly by the next launch), so every step is
+steady-state work over the whole mix; the warm-up launches start the
+instances. Events per step are measured from the device counters. flow-events = RunResult::events
 (engine.cpp:611), summed over instances.
 
   value : events / device time of the timed launches (inputs resident in HBM,
@@ -44,8 +45,8 @@ def parse():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--instances", type=int, default=int(os.environ.get("MFSIM_BENCH_INSTANCES", 1184)),
                     help="resident instances per rank")
-    ap.add_argument("--budget", type=int, default=20000,
-                    help="events each instance advances per step (launch)")
+    ap.add_argument("--slice-ms", type=float, default=1000.0,
+                    help="device time per step (launch): every warp advances its instance until then")
     ap.add_argument("--requests", type=int, default=2000, help="requests per instance (configs[3]: 2000)")
     ap.add_argument("--cpu-sample-s", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -199,7 +200,8 @@ def workload_config(args):
                     "16 units x 4 hosts + 64 decode, cells = load {0.3..0.9} x SLO {1..5} x "
                     "seed {1..64} x policy {fs,sjf,edf,karuna,mfs}",
         "instances_per_rank": args.instances,
-        "events_per_instance_per_step": args.budget,
+        "step": f"one launch = {args.slice_ms:g} ms of device time per warp (time-sliced, "
+                "instances suspend to HBM and resume exactly)",
         "requests_per_instance": args.requests,
         "l2": "inputs larger than L2 (per-step working set >> 126 MB)",
         "parallelism": f"instance-sharded x{args.gpus}",
@@ -248,7 +250,7 @@ def main():
 
     # warm-up: the first budgeted launches start every instance
     for _ in range(args.warmup):
-        batch.launch_budget(args.budget)
+        batch.launch_slice(int(args.slice_ms * 1e6))
     barrier()
     ev0, by0 = progress()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -256,7 +258,7 @@ def main():
     with Clocks(local) as clk:
         start.record(stream)
         for _ in range(args.steps):
-            batch.launch_budget(args.budget)
+            batch.launch_slice(int(args.slice_ms * 1e6))
         end.record(stream)
         barrier()
     dev_ms = start.elapsed_time(end)
@@ -267,7 +269,7 @@ def main():
     e0 = time.perf_counter()
     for _ in range(args.steps):
         batch.upload_inputs()
-        batch.launch_budget(args.budget)
+        batch.launch_slice(int(args.slice_ms * 1e6))
         batch.download(0)
     barrier()
     e2e_s = time.perf_counter() - e0

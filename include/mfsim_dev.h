@@ -77,6 +77,9 @@ int mfsim_dev_reset(mfsim_dev* d);
 /* advance every unfinished instance by at most `budget` events (suspended
  * instances resume exactly where they stopped); returns immediately */
 int mfsim_dev_launch_budget(mfsim_dev* d, long long budget);
+/* advance every unfinished instance for `slice_ns` nanoseconds of device
+ * time (all warps stop at the same deadline and suspend) */
+int mfsim_dev_launch_slice(mfsim_dev* d, long long slice_ns);
 /* instances not finished yet (synchronises the stream) */
 int mfsim_dev_remaining(mfsim_dev* d);
 /* wait for the stream; *kernel_ms receives the last launch's device time */

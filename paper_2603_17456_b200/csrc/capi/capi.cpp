@@ -220,6 +220,11 @@ int mfsim_dev_launch_budget(mfsim_dev* d, long long budget) {
   return guarded([&] { d->batch->launch(budget); });
 }
 
+int mfsim_dev_launch_slice(mfsim_dev* d, long long slice_ns) {
+  if (!d || !d->batch) return fail(MFSIM_ERR_INVALID_ARG, "mfsim_dev_launch_slice: nothing prepared");
+  return guarded([&] { d->batch->launch(0, slice_ns); });
+}
+
 int mfsim_dev_remaining(mfsim_dev* d) {
   if (!d || !d->batch) return -1;
   int r = -1;

@@ -76,6 +76,16 @@ MF_FN unsigned long long dbits(double x) {
 MF_FN bool isnan_(double x) { return x != x; }
 #endif
 #if defined(__CUDACC__)
+MF_FN unsigned long long now_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#else
+MF_FN unsigned long long now_ns() { return 0; }
+#endif
+
+#if defined(__CUDACC__)
 MF_FN double bits_to_d(unsigned long long u) { return __longlong_as_double((long long)u); }
 #else
 MF_FN double bits_to_d(unsigned long long u) {
@@ -2881,9 +2891,9 @@ struct Engine {
   }
 
   // Runs the instance's event loop for at most `budget` events (<= 0: to the
-  // end). A suspended instance keeps all state in HBM plus its scalar state in
+  // end) and, with deadline_ns, until the device clock passes it. A suspended instance keeps all state in HBM plus its scalar state in
   // sc_blob and resumes exactly where it stopped. Returns true when finished.
-  MF_NOINLINE bool run(long long budget) {
+  MF_NOINLINE bool run(long long budget, unsigned long long deadline_ns = 0) {
     static_assert(sizeof(Sc) <= kScBlob, "scalar state exceeds its blob");
     const int ph = *I.phase;
     if (ph == 2) return false;
@@ -2901,6 +2911,7 @@ struct Engine {
     bool finished = false;
     while (!s.err) {
       if (s.events >= stop_at) break;
+      if (deadline_ns && now_ns() >= deadline_ns) break;
       MF_TIC(tn);
       Ev e = next_event();
       MF_TOC(OUT_CY_NEXT, tn);

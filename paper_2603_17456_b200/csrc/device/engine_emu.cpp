@@ -28,7 +28,8 @@ class EmuBackend final : public Backend {
   void d2h(void* h, const void* d, size_t n) override {
     if (n) std::memcpy(h, d, n);
   }
-  void launch(const mfb::Inst* d, const int*, int n, const LaunchHint&, long long budget) override {
+  void launch(const mfb::Inst* d, const int*, int n, const LaunchHint&, long long budget,
+              long long) override {
     for (int i = 0; i < n; ++i) {
       mfb::Inst local = d[i];
       mfb::Engine<mfb::SerialLanes, false, false> eng(local);

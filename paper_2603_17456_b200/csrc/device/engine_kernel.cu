@@ -48,10 +48,18 @@ __host__ inline SmemPlan make_plan(int nlinks) {
 __global__ void __launch_bounds__(32)
     mfsim_engine_kernel(const Inst* __restrict__ insts, const int* __restrict__ order, int n,
                         int* __restrict__ next, SmemPlan plan, long long budget,
-                        int* __restrict__ remaining) {
+                        long long slice_ns, int* __restrict__ remaining) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31;
   Inst* d = reinterpret_cast<Inst*>(smem);
+  // time-sliced launches: every warp works until the same device-clock deadline
+  unsigned long long deadline = 0;
+  if (slice_ns > 0) {
+    __shared__ unsigned long long t0;
+    if (lane == 0) t0 = now_ns();
+    __syncwarp();
+    deadline = t0 + (unsigned long long)slice_ns;
+  }
   for (;;) {
     int i = 0;
     if (lane == 0) i = atomicAdd(next, 1);
@@ -109,10 +117,10 @@ __global__ void __launch_bounds__(32)
     bool done;
     if (slots_on_chip) {
       Engine<WarpLanes, false, true> eng(*d);
-      done = eng.run(budget);
+      done = eng.run(budget, deadline);
     } else {
       Engine<WarpLanes, false, false> eng(*d);
-      done = eng.run(budget);
+      done = eng.run(budget, deadline);
     }
     if (done && lane == 0) atomicSub(remaining, 1);
     __syncwarp();
@@ -173,7 +181,7 @@ class CudaBackend final : public Backend {
     if (n) ck(cudaMemcpyAsync(h, d, n, cudaMemcpyDeviceToHost, stream_), "D2H");
   }
   void launch(const mfb::Inst* d, const int* order, int n, const LaunchHint& hint,
-              long long budget) override {
+              long long budget, long long slice_ns) override {
     const mfb::SmemPlan plan = mfb::make_plan(hint.nlinks);
     int per_sm = 0;
     ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mfb::mfsim_engine_kernel, 32,
@@ -185,7 +193,7 @@ class CudaBackend final : public Backend {
     ck(cudaMemsetAsync(counter_, 0, sizeof(int), stream_), "memset");
     ck(cudaEventRecord(e0_, stream_), "event");
     mfb::mfsim_engine_kernel<<<grid, 32, plan.bytes, stream_>>>(d, order, n, counter_, plan,
-                                                                budget, counter_ + 1);
+                                                                budget, slice_ns, counter_ + 1);
     ck(cudaGetLastError(), "launch");
     ck(cudaEventRecord(e1_, stream_), "event");
     ++launches_;

@@ -932,7 +932,9 @@ void Batch::reset() {
   be_.set_remaining(size());
 }
 
-void Batch::launch(long long budget) { be_.launch(desc_dev_, order_dev_, size(), hint_, budget); }
+void Batch::launch(long long budget, long long slice_ns) {
+  be_.launch(desc_dev_, order_dev_, size(), hint_, budget, slice_ns);
+}
 
 int Batch::remaining() { return be_.remaining(); }
 

@@ -47,7 +47,7 @@ class Backend {
   // order: device array, a permutation of [0, n) giving the claim order;
   // budget: events per instance in this launch (<= 0: run to completion)
   virtual void launch(const mfb::Inst* d_insts, const int* order, int n, const LaunchHint& hint,
-                      long long budget) = 0;
+                      long long budget, long long slice_ns) = 0;
   virtual void set_remaining(int n) = 0;
   virtual int remaining() = 0;
   virtual void sync() = 0;
@@ -121,7 +121,9 @@ class Batch {
   void upload();          // H2D of all inputs (stream-ordered) + reset()
   void upload_inputs();   // H2D of the inputs only (state untouched)
   void reset();           // every instance back to its initial state (fresh run)
-  void launch(long long budget = 0);  // device event loops (stream-ordered)
+  // device event loops (stream-ordered): at most `budget` events per instance
+  // and, with slice_ns > 0, until that much device time has passed
+  void launch(long long budget = 0, long long slice_ns = 0);
   int remaining();        // instances not finished yet (synchronises)
   void download(int detail);  // D2H; detail 0 requests, 1 +coflows, 2 +flows/batches
   // upload + launch + download, re-running instances that hit a capacity

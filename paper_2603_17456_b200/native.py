@@ -113,7 +113,7 @@ class Native:
             "mfsim_route": ([vp, i, i, vp, vp, i, C.POINTER(i)], i),
             "mfsim_dev_counters": ([vp, i, vp, i], i),
             "mfsim_dev_reset": ([vp], i), "mfsim_dev_upload_inputs": ([vp], i), "mfsim_dev_launch_budget": ([vp, ll], i),
-            "mfsim_dev_remaining": ([vp], i),
+            "mfsim_dev_remaining": ([vp], i), "mfsim_dev_launch_slice": ([vp, ll], i),
             "mfsim_link_count": ([vp, C.POINTER(i)], i),
         }
         for name, (args, res) in sig.items():
@@ -223,6 +223,9 @@ class DeviceBatch:
 
     def launch_budget(self, budget: int):
         self.n.check(self.n.lib.mfsim_dev_launch_budget(self.h, budget))
+
+    def launch_slice(self, slice_ns: int):
+        self.n.check(self.n.lib.mfsim_dev_launch_slice(self.h, slice_ns))
 
     def remaining(self) -> int:
         return self.n.lib.mfsim_dev_remaining(self.h)
