@@ -347,27 +347,33 @@ InstanceInput workload_instance(const Config& cfg) {
 }
 
 void derive_deadlines(Backend& be, const std::vector<InstanceInput*>& insts) {
-  // one isolated run per distinct key per instance (workload.cpp:199-217)
+  // One isolated run per distinct key (workload.cpp:199-217). The run depends
+  // only on the fabric, the engine/cost parameters and the key, so identical
+  // probes of different instances (seeds, loads, SLO scales, policies of one
+  // sweep) are simulated once.
   std::vector<InstanceInput> probes;
   std::vector<std::vector<int>> probe_of(insts.size());
+  std::map<std::tuple<const void*, std::string, long, long, int, int>, int> cache;
   for (size_t i = 0; i < insts.size(); ++i) {
     InstanceInput& in = *insts[i];
-    std::map<std::tuple<long, long, int, int>, int> cache;
+    InstParams fsp = in.p;
+    FairShareScheduler fs;
+    fs.configure(fsp);
+    fsp.horizon = 0.0 + 1e9;  // horizon reset, slack 1e9 (workload.cpp:189-191)
+    std::string pkey(reinterpret_cast<const char*>(&fsp), sizeof(fsp));
     probe_of[i].resize(in.reqs.size());
     for (size_t r = 0; r < in.reqs.size(); ++r) {
       const HostRequest& q = in.reqs[r];
       const long bits = static_cast<long>(std::llround(q.reuse * 1e9));
-      auto key = std::make_tuple(q.tokens, bits, q.unit, q.source);
+      auto key = std::make_tuple(static_cast<const void*>(in.topo.get()), pkey, q.tokens, bits, q.unit,
+                                 q.source);
       auto it = cache.find(key);
       if (it != cache.end()) {
         probe_of[i][r] = it->second;
         continue;
       }
       InstanceInput p;
-      p.p = in.p;
-      FairShareScheduler fs;
-      fs.configure(p.p);
-      p.p.horizon = 0.0 + 1e9;  // horizon reset, slack 1e9 (workload.cpp:189-191)
+      p.p = fsp;
       p.topo = in.topo;
       HostRequest pr = q;
       pr.arrival = 0.0;
