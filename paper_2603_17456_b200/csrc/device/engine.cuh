@@ -157,7 +157,7 @@ struct Sc {
   int n_live;
   int h_n, h_ready;
   int n_srt, n_add;
-  int n_slots;
+  int sl_hw, sl_nfree, n_unslotted;
   bool bk_slots;
   int bk_n;
   bool rel_idx;
@@ -336,6 +336,29 @@ struct Engine {
   MF_FN void remove_active_at(int fid, int pos) {
     const int last = s.n_active - 1;
     const int lf = I.a_fid[last];
+    if (I.TS_cap > 0) {  // the leaving flow releases its route's slots
+      int nf = s.sl_nfree, un = s.n_unslotted;
+      g.sync();
+      if (g.leader()) {
+        const int rn = I.a_rn[pos];
+        for (int k = 0; k < rn; ++k) {
+          const int sl = I.a_sl[pos * I.rmax + k];
+          if (sl == 0xFFFF) {
+            --un;
+            continue;
+          }
+          const int ref = I.sl_ref[sl] - 1;
+          I.sl_ref[sl] = (unsigned short)ref;
+          if (ref == 0) {
+            I.l2s[I.sl_link[sl]] = 0xFFFFu;
+            I.sl_free[nf++] = (unsigned short)sl;
+          }
+        }
+      }
+      g.sync();
+      s.sl_nfree = g.shfl(nf, 0);
+      s.n_unslotted = g.shfl(un, 0);
+    }
     g.sync();
     if (g.leader()) {
       I.a_fid[pos] = lf;
@@ -348,7 +371,10 @@ struct Engine {
       I.f_apos[fid] = -1;
     }
     const int rm = I.rmax;
-    for (int k = g.lane(); k < rm; k += G::N) I.a_rl[pos * rm + k] = I.a_rl[last * rm + k];
+    for (int k = g.lane(); k < rm; k += G::N) {
+      I.a_rl[pos * rm + k] = I.a_rl[last * rm + k];
+      I.a_sl[pos * rm + k] = I.a_sl[last * rm + k];
+    }
     g.sync();
     --s.n_active;
   }
@@ -448,77 +474,24 @@ struct Engine {
     return I.p.K;
   }
 
-  // Stable bucketing by link of n entries (link x_seg[e], key x_hi[e], value
-  // x_val[e]) into y_key / y_val: a warp counting sort whose scatter ranks
-  // equal links by lane (match_any), so each link's bucket keeps entry order.
-  // The buckets of the distinct links are addressed through compact slots
-  // (l2s map + sl_cnt / sl_mb / sl_end, on chip) when they fit TS_cap, else
-  // through the per-link arrays (l_cnt / l_off). Query a link's bucket with
-  // bucket_of(); bucket_release() clears the state.
+  // Stable bucketing of n entries (route position x_seg[e] = slot id in slot
+  // mode, link id otherwise; key x_hi[e]; value x_val[e]; payload x_aux[e])
+  // into y_key / y_val / y_aux: a warp counting sort whose scatter ranks equal
+  // keys by lane (match_any), so each bucket keeps entry order. Slot mode uses
+  // the on-chip per-slot counters; link mode the per-link arrays in HBM.
+  // Query a bucket with bucket_at() / bucket_of(); bucket_release() after.
+  MF_FN bool slot_mode() const { return I.TS_cap > 0 && s.n_unslotted == 0; }
+  MF_FN int entry_key(int p, int k) const { return slot_mode() ? I.a_sl[p * I.rmax + k] : arl(p, k); }
+
   MF_FN int bucket_by_link(int n) {
-    s.bk_slots = false;
-    if (I.TS_cap > 0) {
-      // claim a slot per distinct link
-      unsigned short* __restrict__ l2s = I.l2s;
-      int ns = 0;
-      for (int base = 0; base < n; base += G::N) {
-        const int e = base + g.lane();
-        const bool has = e < n;
-        const int l = has ? I.x_seg[e] : -1 - g.lane();
-        const unsigned peers = g.match_any(l);
-        const bool fresh = has && (peers & g.lanemask_lt()) == 0u && l2s[l] == 0xFFFFu;
-        const unsigned m = g.ballot(fresh);
-        if (fresh) {
-          const int sl = ns + popc32(m & g.lanemask_lt());
-          l2s[l] = (unsigned short)(sl < I.TS_cap ? sl : 0xFFFEu);
-          if (sl < I.TS_cap) {
-            I.sl_link[sl] = (unsigned short)l;
-            I.sl_cnt[sl] = 0;
-          }
-          I.x_lo[sl] = (unsigned long long)l;  // claimed links (for the overflow reset)
-        }
-        ns += popc32(m);
-        g.sync();
-      }
-      if (ns <= I.TS_cap) {
-        s.bk_slots = true;
-        s.bk_n = ns;
-        for (int e = g.lane(); e < n; e += G::N) g.atomic_add(&I.sl_cnt[l2s[I.x_seg[e]]], 1);
-        g.sync();
-        int off = 0;
-        for (int base = 0; base < ns; base += G::N) {
-          const int j = base + g.lane();
-          const int c = j < ns ? I.sl_cnt[j] : 0;
-          int tot;
-          const int o = g.excl_scan(c, &tot);
-          if (j < ns) {
-            I.sl_mb[j] = (unsigned short)(off + o);
-            I.sl_end[j] = (unsigned short)(off + o);
-          }
-          off += tot;
-        }
-        g.sync();
-        for (int base = 0; base < n; base += G::N) {
-          const int e = base + g.lane();
-          const int sl = e < n ? (int)l2s[I.x_seg[e]] : -1 - g.lane();
-          const unsigned peers = g.match_any(sl);
-          int pos = 0;
-          if (e < n) {
-            pos = I.sl_end[sl] + popc32(peers & g.lanemask_lt());
-            I.y_key[pos] = I.x_hi[e];
-            I.y_val[pos] = I.x_val[e];
-            I.y_aux[pos] = I.x_aux[e];
-          }
-          g.sync();
-          if (e < n && (peers >> g.lane()) == 1u) I.sl_end[sl] = (unsigned short)(pos + 1);
-          g.sync();
-        }
-        return ns;
-      }
-      for (int j = g.lane(); j < ns; j += G::N) l2s[(int)I.x_lo[j]] = 0xFFFFu;
+    s.bk_slots = slot_mode();
+    int* cntp = s.bk_slots ? I.sl_cnt : I.l_cnt;
+    int* offp = s.bk_slots ? I.sl_end : I.l_off;
+    unsigned short* tlp = s.bk_slots ? I.sl_tl : I.s_tl;
+    if (s.bk_slots) {
+      for (int j = g.lane(); j < s.sl_hw; j += G::N) I.sl_cnt[j] = 0;
       g.sync();
     }
-    // per-link global arrays
     int nt = 0;
     for (int base = 0; base < n; base += G::N) {
       const int e = base + g.lane();
@@ -526,10 +499,10 @@ struct Engine {
       int l = 0;
       if (e < n) {
         l = I.x_seg[e];
-        first = g.atomic_add(&I.l_cnt[l], 1) == 0;
+        first = g.atomic_add(&cntp[l], 1) == 0;
       }
       const unsigned m = g.ballot(first);
-      if (first) I.s_tl[nt + popc32(m & g.lanemask_lt())] = (unsigned short)l;
+      if (first) tlp[nt + popc32(m & g.lanemask_lt())] = (unsigned short)l;
       nt += popc32(m);
     }
     g.sync();
@@ -538,12 +511,15 @@ struct Engine {
       const int j = base + g.lane();
       int c = 0, l = 0;
       if (j < nt) {
-        l = I.s_tl[j];
-        c = I.l_cnt[l];
+        l = tlp[j];
+        c = cntp[l];
       }
       int tot;
       const int o = g.excl_scan(c, &tot);
-      if (j < nt) I.l_off[l] = off + o;
+      if (j < nt) {
+        offp[l] = off + o;
+        if (s.bk_slots) I.sl_mb[l] = off + o;
+      }
       off += tot;
     }
     g.sync();
@@ -551,36 +527,38 @@ struct Engine {
       const int e = base + g.lane();
       const int l = e < n ? I.x_seg[e] : -1 - g.lane();
       const unsigned peers = g.match_any(l);
+      int pos = 0;
       if (e < n) {
-        const int pos = I.l_off[l] + popc32(peers & g.lanemask_lt());
+        pos = offp[l] + popc32(peers & g.lanemask_lt());
         I.y_key[pos] = I.x_hi[e];
         I.y_val[pos] = I.x_val[e];
         I.y_aux[pos] = I.x_aux[e];
       }
       g.sync();
-      if (e < n && (peers >> g.lane()) == 1u) I.l_off[l] += popc32(peers);
+      if (e < n && (peers >> g.lane()) == 1u) offp[l] = pos + 1;
       g.sync();
     }
     s.bk_n = nt;
     return nt;
   }
-  // j-th bucketed link and its entry range [*e0, *e1)
+  // j-th bucket: its link and entry range [*e0, *e1)
   MF_FN int bucket_at(int j, int* e0, int* e1) const {
     if (s.bk_slots) {
-      *e0 = I.sl_mb[j];
-      *e1 = I.sl_end[j];
-      return I.sl_link[j];
+      const int sl = I.sl_tl[j];
+      *e0 = I.sl_mb[sl];
+      *e1 = I.sl_end[sl];
+      return I.sl_link[sl];
     }
     const int l = I.s_tl[j];
     *e1 = I.l_off[l];
     *e0 = *e1 - I.l_cnt[l];
     return l;
   }
-  // entry range of link l (empty when l has no entries)
+  // entry range of link l (false when l has no entries)
   MF_FN bool bucket_of(int l, int* e0, int* e1) const {
     if (s.bk_slots) {
       const int sl = I.l2s[l];
-      if (sl == 0xFFFF) return false;
+      if (sl == 0xFFFF || I.sl_cnt[sl] == 0) return false;
       *e0 = I.sl_mb[sl];
       *e1 = I.sl_end[sl];
       return true;
@@ -593,7 +571,7 @@ struct Engine {
   }
   MF_FN void bucket_release(int nt) {
     if (s.bk_slots) {
-      for (int j = g.lane(); j < nt; j += G::N) I.l2s[I.sl_link[j]] = 0xFFFFu;
+      for (int j = g.lane(); j < nt; j += G::N) I.sl_cnt[I.sl_tl[j]] = 0;
     } else {
       for (int j = g.lane(); j < nt; j += G::N) I.l_cnt[I.s_tl[j]] = 0;
     }
@@ -617,7 +595,7 @@ struct Engine {
         const double r = I.a_rate[p];
         const int hx = I.f_hidx[fid];
         for (int k = 0; k < c; ++k) {
-          I.x_seg[n + off + k] = arl(p, k);
+          I.x_seg[n + off + k] = entry_key(p, k);
           I.x_hi[n + off + k] = key;
           I.x_val[n + off + k] = r;
           I.x_aux[n + off + k] = hx;
@@ -1312,7 +1290,7 @@ struct Engine {
       const int off = g.excl_scan(c, &tot);
       if (c > 0) {
         for (int k = 0; k < c; ++k) {
-          I.x_seg[n + off + k] = arl(p, k);
+          I.x_seg[n + off + k] = entry_key(p, k);
           I.x_hi[n + off + k] = 0;
           I.x_val[n + off + k] = want;
           I.x_aux[n + off + k] = 0;
@@ -1361,55 +1339,10 @@ struct Engine {
   // freeze permanently), which equals the reference's per-round recount; the
   // rounds then touch only that class's links and its unfrozen members.
   MF_FN void allocate(int ncls, bool has_caps) {
-    if (I.TS_cap > 0 && build_slots())
+    if (I.TS_cap > 0 && s.n_unslotted == 0)
       allocate_slots(ncls, has_caps);
     else
       allocate_generic(ncls, has_caps);
-  }
-
-  // Compact slots for the links of every active route (this step): a slot per
-  // distinct link, residual initialised to the capacity (allocator.cpp:36-37).
-  // Returns false (and leaves l2s clear) when they exceed TS_cap.
-  MF_NOINLINE bool build_slots() {
-    const int A = s.n_active;
-    const int RM = I.rmax;
-    unsigned short* __restrict__ l2s = I.l2s;
-    unsigned short* __restrict__ asl = I.a_sl;
-    int* __restrict__ claimed = I.x_seg;  // every claimed link, for the reset
-    int ns = 0;
-    for (int base = 0; base < A; base += G::N) {
-      const int p = base + g.lane();
-      const int rn = p < A ? (int)I.a_rn[p] : 0;
-      for (int k = 0; k < RM; ++k) {
-        const bool has = k < rn;
-        const int l = has ? (int)I.a_rl[p * RM + k] : -1 - g.lane();
-        const unsigned peers = g.match_any(l);
-        const bool lead = has && (peers & g.lanemask_lt()) == 0u;
-        const bool fresh = lead && l2s[l] == 0xFFFFu;
-        const unsigned m = g.ballot(fresh);
-        if (fresh) {
-          const int sl = ns + popc32(m & g.lanemask_lt());
-          claimed[sl] = l;
-          l2s[l] = (unsigned short)(sl < I.TS_cap ? sl : 0xFFFEu);
-          if (sl < I.TS_cap) {
-            I.sl_link[sl] = (unsigned short)l;
-            I.sl_res[sl] = I.cap[l];
-            I.sl_cnt[sl] = 0;
-          }
-        }
-        ns += popc32(m);
-        g.sync();
-        if (has) asl[p * RM + k] = l2s[l];
-      }
-    }
-    g.sync();
-    if (ns > I.TS_cap) {
-      for (int j = g.lane(); j < ns; j += G::N) l2s[claimed[j]] = 0xFFFFu;
-      g.sync();
-      return false;
-    }
-    s.n_slots = ns;
-    return true;
   }
 
   // per-member rounds over global-memory arrays (instances beyond the
@@ -1599,25 +1532,37 @@ struct Engine {
     s.algo_bytes += bytes;
   }
 
-  // class filling with the shared class rate over compact link slots
+  // class filling with the shared class rate over the link slots
   MF_NOINLINE void allocate_slots(int ncls, bool has_caps) {
     const int A = s.n_active;
     const int RM = I.rmax;
+    const int hw = s.sl_hw;
     int* __restrict__ ord = I.s_ord;
     const int* __restrict__ afid = I.a_fid;
-    const unsigned short* __restrict__ arlp = I.a_sl;  // slot ids
+    const unsigned short* __restrict__ asl = I.a_sl;
     const uint8_t* __restrict__ arnp = I.a_rn;
     double* __restrict__ res = I.sl_res;
     int* __restrict__ cnt = I.sl_cnt;
-    double* __restrict__ rate = I.s_rate;
-    int* __restrict__ ul = I.s_ul;
+    int* __restrict__ mb = I.sl_mb;
+    int* __restrict__ mend = I.sl_end;
     unsigned short* __restrict__ tl = I.sl_tl;
+    unsigned short* __restrict__ sat = I.sl_sat;
+    double* __restrict__ rate = I.s_rate;
     const double* __restrict__ capv = I.cap;
     const unsigned short* __restrict__ slink = I.sl_link;
     const double* __restrict__ scap = I.s_cap;
+    unsigned short* __restrict__ mem = I.c_mem;
+    uint8_t* __restrict__ frz = I.c_frz;
+    if (kLinksOnChip) {
+      MF_SH(res);
+      MF_SH(cnt);
+      MF_SH(mb);
+      MF_SH(mend);
+      MF_SH(tl);
+      MF_SH(sat);
+    }
     MF_TIC(q0);
-    // rate-map insertion order for the load_fraction hash emulation
-    {
+    if (I.p.policy == POL_MFS) {  // rate-map insertion order (load_fraction)
       int* __restrict__ hk = I.h_keys;
       int* __restrict__ hidx = I.f_hidx;
       for (int i = g.lane(); i < A; i += G::N) {
@@ -1625,11 +1570,16 @@ struct Engine {
         hk[i] = fid;
         hidx[fid] = i;
       }
+      s.h_n = A;
+      s.h_ready = 0;
+    }
+    // residual = capacity on every slot (allocator.cpp:36-37), counts zero
+    for (int j = g.lane(); j < hw; j += G::N) {
+      res[j] = capv[slink[j]];
+      cnt[j] = 0;
     }
     g.sync();
     MF_TOC(OUT_CY_SUB + 0, q0);
-    s.h_n = A;
-    s.h_ready = 0;
     long long rounds = 0, bytes = 0;
     for (int c = 0; c < ncls; ++c) {
       const int o0 = I.s_cls[c], o1 = I.s_cls[c + 1];
@@ -1643,13 +1593,13 @@ struct Engine {
           if (cp < MF_INF) r = smax(0.0, cp);
         }
         double mine = MF_INF;
-        for (int k = g.lane(); k < rn; k += G::N) mine = smin(mine, smax(0.0, res[arlp[p * RM + k]]));
+        for (int k = g.lane(); k < rn; k += G::N) mine = smin(mine, smax(0.0, res[asl[p * RM + k]]));
         for (int m = G::N / 2; m > 0; m >>= 1) mine = smin(mine, g.shfl_xor(mine, m));
         r = smin(r, mine);
         g.sync();
         for (int k = g.lane(); k < rn; k += G::N) {
-          const int l = arlp[p * RM + k];
-          res[l] = dsub(res[l], r);
+          const int j = asl[p * RM + k];
+          res[j] = dsub(res[j], r);
         }
         if (g.leader()) rate[p] = r;
         g.sync();
@@ -1659,24 +1609,13 @@ struct Engine {
       // multi-flow class (allocator.cpp:61-121). Every unfrozen member has
       // received the same sequence of increments from 0, so they share one
       // rate R; a member's rate is R at the round it freezes. Per round:
-      //   inc = max(min(min_l max(0,res_l)/cnt_l, capmin - R), 0)
-      //   R += inc; res_l -= inc * cnt_l on links with unfrozen members
+      //   inc = max(min(min_j max(0,res_j)/cnt_j, capmin - R), 0)
+      //   R += inc; res_j -= inc * cnt_j on slots with unfrozen members
       //   freeze members with R >= cap - eps (a prefix of the cap order,
       //   since cap - 1e-12*max(1,cap) is increasing in cap) and members of
-      //   links whose residual fell to <= 1e-12 * capacity.
+      //   slots whose residual fell to <= 1e-12 * capacity.
       MF_TIC(q1);
-      unsigned short* __restrict__ mem = I.c_mem;
-      unsigned short* __restrict__ mb = I.sl_mb;
-      unsigned short* __restrict__ mend = I.sl_end;
-      unsigned short* __restrict__ sat = I.sl_sat;
-      uint8_t* __restrict__ frz = I.c_frz;
-      if (kLinksOnChip) {
-        MF_SH(mb);
-        MF_SH(mend);
-        MF_SH(sat);
-      }
-      int nt = 0;
-      int ncap = 0;
+      int nt = 0, ncap = 0;
       for (int base = 0; base < n; base += G::N) {
         const int i = base + g.lane();
         int p = 0, rn = 0;
@@ -1689,13 +1628,13 @@ struct Engine {
         }
         for (int k = 0; k < RM; ++k) {
           bool first = false;
-          int l = 0;
+          int j = 0;
           if (k < rn) {
-            l = arlp[p * RM + k];
-            first = g.atomic_add(&cnt[l], 1) == 0;
+            j = asl[p * RM + k];
+            first = g.atomic_add(&cnt[j], 1) == 0;
           }
           const unsigned m = g.ballot(first);
-          if (first) tl[nt + popc32(m & g.lanemask_lt())] = (unsigned short)l;
+          if (first) tl[nt + popc32(m & g.lanemask_lt())] = (unsigned short)j;
           nt += popc32(m);
         }
         const unsigned mc = g.ballot(capped);
@@ -1707,47 +1646,30 @@ struct Engine {
         ncap += popc32(mc);
       }
       g.sync();
-      // link -> member incidence: extents from the counts, then a stable fill
-      // (equal links within a chunk ranked by lane, so no 16-bit atomics)
-      {
+      {  // slot -> member incidence: extents from the counts, atomic fill
         int off = 0;
         for (int base = 0; base < nt; base += G::N) {
-          const int j = base + g.lane();
-          int c0 = 0, l = 0;
-          if (j < nt) {
-            l = tl[j];
-            c0 = cnt[l];
+          const int jj = base + g.lane();
+          int c0 = 0, j = 0;
+          if (jj < nt) {
+            j = tl[jj];
+            c0 = cnt[j];
           }
           int tot;
           const int o = g.excl_scan(c0, &tot);
-          if (j < nt) {
-            mb[l] = (unsigned short)(off + o);
-            mend[l] = (unsigned short)(off + o);
+          if (jj < nt) {
+            mb[j] = off + o;
+            mend[j] = off + o;
           }
           off += tot;
         }
         g.sync();
-        for (int base = 0; base < n; base += G::N) {
-          const int i = base + g.lane();
-          int p = 0, rn = 0;
-          if (i < n) {
-            p = ord[o0 + i];
-            rn = arnp[p];
-          }
-          for (int k = 0; k < RM; ++k) {
-            const bool has = k < rn;
-            const int l = has ? (int)arlp[p * RM + k] : -1 - g.lane();
-            const unsigned peers = g.match_any(l);
-            int pos = 0;
-            if (has) {
-              pos = mend[l] + popc32(peers & g.lanemask_lt());
-              mem[pos] = (unsigned short)p;
-            }
-            g.sync();
-            if (has && (peers >> g.lane()) == 1u) mend[l] = (unsigned short)(pos + 1);
-            g.sync();
-          }
+        for (int i = g.lane(); i < n; i += G::N) {
+          const int p = ord[o0 + i];
+          const int rn = arnp[p];
+          for (int k = 0; k < rn; ++k) mem[g.atomic_add(&mend[asl[p * RM + k]], 1)] = (unsigned short)p;
         }
+        g.sync();
       }
       if (ncap > 1) sort_caps(ncap);  // caps ascending (cap >= 0: bit order)
       MF_TOC(OUT_CY_SUB + 1, q1);
@@ -1758,15 +1680,14 @@ struct Engine {
       while (nu > 0) {
         ++rounds;
         MF_TIC(q2);
-        // capmin over unfrozen capped members (frozen ones skipped lazily)
         while (cptr < ncap && frz[(int)I.x_lo[cptr]]) ++cptr;
         const double cmin = cptr < ncap ? dsub(bits_to_d(I.x_hi[cptr]), R) : MF_INF;
         double amin = MF_INF;
 #pragma unroll 4
-        for (int j = g.lane(); j < nt; j += G::N) {
-          const int l = tl[j];
-          const int cn = cnt[l];
-          const double r = res[l];
+        for (int jj = g.lane(); jj < nt; jj += G::N) {
+          const int j = tl[jj];
+          const int cn = cnt[j];
+          const double r = res[j];
           if (cn > 0) amin = smin(amin, dmul(smax(0.0, r), frecip(cn)));
         }
         for (int m = G::N / 2; m > 0; m >>= 1) amin = smin(amin, g.shfl_xor(amin, m));
@@ -1774,10 +1695,10 @@ struct Engine {
         if (amin <= cmin) {  // exact quotients only within the approximation margin
           const double athr = dadd(amin, dmul(amin, 0x1p-18));
 #pragma unroll 4
-          for (int j = g.lane(); j < nt; j += G::N) {
-            const int l = tl[j];
-            const int cn = cnt[l];
-            const double r = smax(0.0, res[l]);
+          for (int jj = g.lane(); jj < nt; jj += G::N) {
+            const int j = tl[jj];
+            const int cn = cnt[j];
+            const double r = smax(0.0, res[j]);
             if (cn > 0 && dmul(r, frecip(cn)) <= athr) inc = smin(inc, ddiv(r, (double)cn));
           }
           for (int m = G::N / 2; m > 0; m >>= 1) inc = smin(inc, g.shfl_xor(inc, m));
@@ -1786,28 +1707,28 @@ struct Engine {
         R = dadd(R, inc);
         MF_TOC(OUT_CY_SUB + 2, q2);
         MF_TIC(q3);
-        // residual update; saturated links collected, drained links dropped
+        // residual update; saturated slots collected, drained slots dropped
         int ns = 0, nt2 = 0;
         for (int base = 0; base < nt; base += G::N) {
-          const int j = base + g.lane();
-          int l = 0;
+          const int jj = base + g.lane();
+          int j = 0;
           bool st = false, live = false;
-          if (j < nt) {
-            l = tl[j];
-            const int cn = cnt[l];
+          if (jj < nt) {
+            j = tl[jj];
+            const int cn = cnt[j];
             if (cn > 0) {
-              const double r = dsub(res[l], dmul(inc, (double)cn));
-              res[l] = r;
-              st = r <= dmul(1e-12, capv[slink[l]]);
+              const double r = dsub(res[j], dmul(inc, (double)cn));
+              res[j] = r;
+              st = r <= dmul(1e-12, capv[slink[j]]);
               live = !st;
             }
           }
-          g.sync();  // all lanes read tl[j] before the in-place compaction
+          g.sync();  // all lanes read tl[jj] before the in-place compaction
           const unsigned ms = g.ballot(st);
-          if (st) sat[ns + popc32(ms & g.lanemask_lt())] = (unsigned short)l;
+          if (st) sat[ns + popc32(ms & g.lanemask_lt())] = (unsigned short)j;
           ns += popc32(ms);
           const unsigned ml = g.ballot(live);
-          if (live) tl[nt2 + popc32(ml & g.lanemask_lt())] = (unsigned short)l;
+          if (live) tl[nt2 + popc32(ml & g.lanemask_lt())] = (unsigned short)j;
           nt2 += popc32(ml);
         }
         g.sync();
@@ -1827,26 +1748,27 @@ struct Engine {
             rate[p] = R;
           }
           const int rn = arnp[p];
-          for (int k = g.lane(); k < rn; k += G::N) g.atomic_add(&cnt[arlp[p * RM + k]], -1);
+          for (int k = g.lane(); k < rn; k += G::N) g.atomic_add(&cnt[asl[p * RM + k]], -1);
           g.sync();
           ++frozen;
         }
-        // link freezes: every unfrozen member of a saturated link (links one
-        // after another; a link lists each member once)
+        // link freezes: every unfrozen member of every saturated slot, all in
+        // one pass (a member on two saturated slots is claimed once)
+        int got = 0;
         for (int q = 0; q < ns; ++q) {
-          const int l = sat[q];
-          const int e0 = mb[l], e1 = mend[l];
-          int got = 0;
-          for (int e = e0 + g.lane(); e < e1; e += G::N) {
+          const int j = sat[q];
+          const int e1 = mend[j];
+          for (int e = mb[j] + g.lane(); e < e1; e += G::N) {
             const int p = mem[e];
-            if (frz[p]) continue;
-            frz[p] = 1;
+            if (frz[p] || g.atomic_exch_u8(&frz[p]) != 0) continue;
             rate[p] = R;
             const int rn = arnp[p];
-            for (int k = 0; k < rn; ++k) g.atomic_add(&cnt[arlp[p * RM + k]], -1);
+            for (int k = 0; k < rn; ++k) g.atomic_add(&cnt[asl[p * RM + k]], -1);
             ++got;
           }
-          g.sync();
+        }
+        g.sync();
+        if (ns > 0) {
           int tot;
           g.excl_scan(got, &tot);
           frozen += tot;
@@ -1860,13 +1782,10 @@ struct Engine {
         nu -= frozen;
         nt = nt2;
       }
-      // any links still counting (none when every member froze) are cleared
-      for (int j = g.lane(); j < nt; j += G::N) cnt[tl[j]] = 0;
+      // slot counts of this class are back to zero (every member froze)
+      for (int jj = g.lane(); jj < nt; jj += G::N) cnt[tl[jj]] = 0;
       g.sync();
     }
-    // clear the link -> slot map for the next step
-    for (int j = g.lane(); j < s.n_slots; j += G::N) I.l2s[slink[j]] = 0xFFFFu;
-    g.sync();
     s.classes += ncls;
     s.rounds += rounds;
     s.algo_bytes += bytes;
@@ -2096,6 +2015,32 @@ struct Engine {
     }
     for (int k = g.lane(); k < rn; k += G::N)
       I.a_rl[pos * I.rmax + k] = (unsigned short)I.route_links[rb + k];
+    if (I.TS_cap > 0) {  // a slot per route link, shared by every user
+      int hw = s.sl_hw, nf = s.sl_nfree, un = s.n_unslotted;
+      g.sync();
+      if (g.leader()) {
+        for (int k = 0; k < rn; ++k) {
+          const int l = I.route_links[rb + k];
+          int sl = I.l2s[l];
+          if (sl == 0xFFFF) {
+            if (nf > 0) sl = I.sl_free[--nf];
+            else if (hw < I.TS_cap) sl = hw++;
+            if (sl != 0xFFFF) {
+              I.l2s[l] = (unsigned short)sl;
+              I.sl_link[sl] = (unsigned short)l;
+              I.sl_ref[sl] = 0;
+            }
+          }
+          if (sl != 0xFFFF) I.sl_ref[sl] = (unsigned short)(I.sl_ref[sl] + 1);
+          else ++un;
+          I.a_sl[pos * I.rmax + k] = (unsigned short)sl;
+        }
+      }
+      g.sync();
+      s.sl_hw = g.shfl(hw, 0);
+      s.sl_nfree = g.shfl(nf, 0);
+      s.n_unslotted = g.shfl(un, 0);
+    }
     if (I.p.policy != POL_FS && s.n_add >= 0) {
       if (s.n_add < I.A_cap) {
         if (g.leader()) I.srt_add[s.n_add] = fid;
@@ -2848,7 +2793,7 @@ struct Engine {
     s.horizon = I.p.horizon;
     s.n_srt = 0;
     s.n_add = 0;
-    s.n_slots = 0;
+    s.sl_hw = s.sl_nfree = s.n_unslotted = 0;
     s.rel_idx = false;
     for (int k = 0; k < 32; ++k) s.cy[k] = 0;
     for (int l = g.lane(); l < I.nlinks; l += G::N) I.l2s[l] = 0xFFFFu;
@@ -2901,7 +2846,6 @@ struct Engine {
       const unsigned int* src = reinterpret_cast<const unsigned int*>(I.sc_blob);
       unsigned int* dst = reinterpret_cast<unsigned int*>(&s);
       for (int w = 0; w < (int)(sizeof(Sc) / 4); ++w) dst[w] = src[w];
-      for (int l = g.lane(); l < I.nlinks; l += G::N) I.l2s[l] = 0xFFFFu;
       g.sync();
       pool_copy(true, s.n_ev);
     } else {

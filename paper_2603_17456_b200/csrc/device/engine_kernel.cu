@@ -35,12 +35,11 @@ __host__ __device__ inline int align16(int x) { return (x + 15) & ~15; }
 __host__ inline SmemPlan make_plan(int nlinks) {
   SmemPlan p{};
   p.ES = mfh::kSmemEvents;
-  p.NL = nlinks <= mfh::kSmemLinks ? nlinks : 0;
-  p.TS = p.NL > 0 ? mfh::kSmemSlots : 0;
+  p.NL = 0;
+  p.TS = mfh::kSmemSlots;
   int b = align16(sizeof(Inst));
   b += align16(p.ES * 8) * 2 + align16(p.ES * 4) * 3;
-  b += align16(p.NL * 2);
-  b += align16(p.TS * 8) + align16(p.TS * 4) + 5 * align16(p.TS * 2);
+  b += align16(p.TS * 8) + 3 * align16(p.TS * 4) + 2 * align16(p.TS * 2);
   p.bytes = align16(b);
   return p;
 }
@@ -99,16 +98,15 @@ __global__ void __launch_bounds__(32)
       } else {
         q += 2 * align16(plan.ES * 8) + 3 * align16(plan.ES * 4);
       }
-      if (plan.NL > 0 && d->nlinks <= plan.NL && d->TS_cap > 0) {
-        d->l2s = reinterpret_cast<unsigned short*>(take(plan.NL * 2));
+      if (plan.TS > 0 && d->TS_cap > 0) {
+        // per-step slot state on chip; the slot bookkeeping stays in HBM
+        // (its capacity bound must not change across suspend / resume)
         d->sl_res = reinterpret_cast<double*>(take(plan.TS * 8));
         d->sl_cnt = reinterpret_cast<int*>(take(plan.TS * 4));
-        d->sl_link = reinterpret_cast<unsigned short*>(take(plan.TS * 2));
-        d->sl_mb = reinterpret_cast<unsigned short*>(take(plan.TS * 2));
-        d->sl_end = reinterpret_cast<unsigned short*>(take(plan.TS * 2));
+        d->sl_mb = reinterpret_cast<int*>(take(plan.TS * 4));
+        d->sl_end = reinterpret_cast<int*>(take(plan.TS * 4));
         d->sl_tl = reinterpret_cast<unsigned short*>(take(plan.TS * 2));
         d->sl_sat = reinterpret_cast<unsigned short*>(take(plan.TS * 2));
-        if (d->TS_cap > plan.TS) d->TS_cap = plan.TS;
         slots_on_chip = true;
       }
     }

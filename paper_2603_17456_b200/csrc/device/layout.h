@@ -208,16 +208,21 @@ struct Inst {
   int* s_ord;       // class order (active positions)
   int* s_cls;       // class start offsets (+1 sentinel)
   int* s_ul;        // unfrozen members of the class being filled
-  // slot filling (engine allocate_slots): the links of this step's active
-  // routes get compact slots; per-slot state is small enough for shared memory
+  // Link slots (engine allocate_slots): every link on the route of an active
+  // flow holds a compact slot while any active flow uses it (refcounted,
+  // assigned at release, freed when the last user leaves). Bookkeeping lives
+  // in HBM; the per-step filling state per slot is small enough for shared
+  // memory. Flows that find no free slot fall back to per-link filling.
   int TS_cap;              // slot capacity (0: always the per-link variant)
-  unsigned short* l2s;     // [nlinks] link -> slot, 0xFFFF = none (kept so)
-  unsigned short* a_sl;    // [A_cap * rmax] slot ids of active routes (this step)
-  double* sl_res;          // [TS] residual
-  int* sl_cnt;             // [TS] unfrozen members of the class being filled
+  unsigned short* l2s;     // [nlinks] link -> slot, 0xFFFF = none
+  unsigned short* a_sl;    // [A_cap * rmax] slot ids of active routes
   unsigned short* sl_link; // [TS] slot -> link
-  unsigned short* sl_mb;   // [TS] class member list start
-  unsigned short* sl_end;  // [TS] class member list end / fill cursor
+  unsigned short* sl_ref;  // [TS] active route entries using the slot
+  unsigned short* sl_free; // [TS] free-slot stack
+  double* sl_res;          // [TS] per-step residual
+  int* sl_cnt;             // [TS] per-step count (unfrozen class members / bucket sizes)
+  int* sl_mb;              // [TS] per-step list start
+  int* sl_end;             // [TS] per-step list end / fill cursor
   unsigned short* sl_tl;   // [TS] live slots of the class
   unsigned short* sl_sat;  // [TS] slots saturated this round
   unsigned short* c_mem;   // [A_cap * rmax] slot -> member incidence

@@ -387,16 +387,27 @@ void derive_deadlines(Backend& be, const std::vector<InstanceInput*>& insts) {
     }
   }
   if (probes.empty()) return;
-  Batch batch(be, std::move(probes));
-  batch.run(0);
+  // memory-bounded chunks of probes (each a tiny single-request instance)
+  std::vector<double> low(probes.size(), -1.0);
+  const size_t chunk = 32768;
+  for (size_t b0 = 0; b0 < probes.size(); b0 += chunk) {
+    const size_t b1 = std::min(probes.size(), b0 + chunk);
+    std::vector<InstanceInput> part(std::make_move_iterator(probes.begin() + b0),
+                                    std::make_move_iterator(probes.begin() + b1));
+    Batch batch(be, std::move(part));
+    batch.run(0);
+    for (size_t k = b0; k < b1; ++k) {
+      const InstanceOutput& o = batch.output(static_cast<int>(k - b0));
+      if (o.ttft.size() != 1 || o.ttft[0] == -1.0)
+        throw InternalError("isolated oracle run did not finish");
+      low[k] = o.ttft[0];
+    }
+  }
   for (size_t i = 0; i < insts.size(); ++i) {
     InstanceInput& in = *insts[i];
     for (size_t r = 0; r < in.reqs.size(); ++r) {
-      const InstanceOutput& o = batch.output(probe_of[i][r]);
-      if (o.ttft.size() != 1 || o.ttft[0] == -1.0)
-        throw InternalError("isolated oracle run did not finish");
       HostRequest& q = in.reqs[r];
-      q.deadline = q.arrival + in.slo_mult * o.ttft[0];
+      q.deadline = q.arrival + in.slo_mult * low[probe_of[i][r]];
     }
     in.deadlines_ready = true;
   }
@@ -685,17 +696,21 @@ void carve_instance(Carver& c, const InstanceInput& in, Inst& d, const Inst& top
   d.s_ul = c.S<int>(nA);
   // slot filling state: host-sized for the global fallback (the kernel stages
   // the per-slot arrays in shared memory when they fit its plan)
-  const size_t nts = std::min<size_t>(nl, nA * d.rmax);
+  // slots: at most the per-warp shared-memory plan (kSmemSlots), so the
+  // bound is the same in HBM and on chip and survives suspend / resume
+  const size_t nts = std::min<size_t>({nl, nA * d.rmax, static_cast<size_t>(kSmemSlots)});
   d.TS_cap = (std::getenv("MFSIM_FORCE_GLOBAL") || nA * d.rmax > 65535) ? 0 : static_cast<int>(nts);
   if (const char* cap = std::getenv("MFSIM_SLOT_CAP"))  // test knob: per-step slot overflow
     d.TS_cap = std::min(d.TS_cap, std::atoi(cap));
   d.l2s = c.S<unsigned short>(nl);
   d.a_sl = c.S<unsigned short>(nA * d.rmax);
+  d.sl_link = c.S<unsigned short>(nts);
+  d.sl_ref = c.S<unsigned short>(nts);
+  d.sl_free = c.S<unsigned short>(nts);
   d.sl_res = c.S<double>(nts);
   d.sl_cnt = c.S<int>(nts);
-  d.sl_link = c.S<unsigned short>(nts);
-  d.sl_mb = c.S<unsigned short>(nts);
-  d.sl_end = c.S<unsigned short>(nts);
+  d.sl_mb = c.S<int>(nts);
+  d.sl_end = c.S<int>(nts);
   d.sl_tl = c.S<unsigned short>(nts);
   d.sl_sat = c.S<unsigned short>(nts);
   d.c_mem = c.S<unsigned short>(nA * d.rmax);
