@@ -102,14 +102,25 @@ class Clocks:
 
 
 def cells_for(rank: int, world: int, n: int, step_offset: int = 0):
-    """rank's slice of the sweep: consecutive chunks of a fixed shuffle of the
-    11,200 cells, so every step mixes loads, SLO scales, seeds and policies"""
+    """rank's slice of the sweep: consecutive chunks of the 11,200 cells ordered
+    seed-major, the 175 (load, SLO scale, policy) cells of one seed in a fixed
+    shuffle. A rank's instances thus mix loads, SLO scales and policies over a
+    few seeds, and share those seeds' isolated-latency probes (derive_slos
+    depends on the seed's requests only, not on the load, SLO scale or policy)."""
     import random
 
     from paper_2603_17456_b200 import sweep
 
     allc = sweep.sweep_cells()
-    random.Random(2603).shuffle(allc)
+    rng = random.Random(2603)
+    blocks = {}
+    for c in allc:
+        blocks.setdefault(c[2], []).append(c)
+    allc = []
+    for seed in sorted(blocks):
+        b = blocks[seed]
+        rng.shuffle(b)
+        allc.extend(b)
     start = ((step_offset * world + rank) * n) % len(allc)
     return [allc[(start + i) % len(allc)] for i in range(n)]
 

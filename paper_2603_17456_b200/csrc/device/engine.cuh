@@ -965,44 +965,6 @@ struct Engine {
       }
     }
   }
-  // ascending (x_hi, x_lo) order of n <= 128 entries: each lane holds up to
-  // four keys in registers and counts smaller keys over the warp (keys are
-  // unique: positions break ties); larger n use the bitonic sort_x
-  MF_FN void sort_caps(int n) {
-    if (n > 4 * G::N) {
-      sort_x(n);
-      return;
-    }
-    unsigned long long kh[4], kl[4];
-    int rk[4];
-#pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      const int j = t * G::N + g.lane();
-      kh[t] = j < n ? I.x_hi[j] : ~0ull;
-      kl[t] = j < n ? I.x_lo[j] : ~0ull;
-      rk[t] = 0;
-    }
-#pragma unroll
-    for (int t2 = 0; t2 < 4; ++t2) {
-      for (int jj = 0; jj < G::N; ++jj) {
-        const unsigned long long oh = g.shfl(kh[t2], jj);
-        const unsigned long long ol = g.shfl(kl[t2], jj);
-#pragma unroll
-        for (int t = 0; t < 4; ++t) rk[t] += (oh < kh[t] || (oh == kh[t] && ol < kl[t])) ? 1 : 0;
-      }
-    }
-    g.sync();
-#pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      const int j = t * G::N + g.lane();
-      if (j < n) {
-        I.x_hi[rk[t]] = kh[t];
-        I.x_lo[rk[t]] = kl[t];
-      }
-    }
-    g.sync();
-  }
-
   // joint sort of x_hi/x_lo/x_val by (hi, lo)
   MF_FN void sort_x(int n) {
     if (n <= 1) return;
@@ -1611,11 +1573,13 @@ struct Engine {
       // rate R; a member's rate is R at the round it freezes. Per round:
       //   inc = max(min(min_j max(0,res_j)/cnt_j, capmin - R), 0)
       //   R += inc; res_j -= inc * cnt_j on slots with unfrozen members
-      //   freeze members with R >= cap - eps (a prefix of the cap order,
-      //   since cap - 1e-12*max(1,cap) is increasing in cap) and members of
-      //   slots whose residual fell to <= 1e-12 * capacity.
+      //   freeze members of slots whose residual fell to <= 1e-12 * capacity
+      //   and members with R >= cap - eps. capmin - R is min_p(cap_p - R)
+      //   (rounding is monotone); the capped unfrozen members are one list,
+      //   compacted and re-minimised by the cap pass of every round.
       MF_TIC(q1);
       int nt = 0, ncap = 0;
+      double cmn = MF_INF;
       for (int base = 0; base < n; base += G::N) {
         const int i = base + g.lane();
         int p = 0, rn = 0;
@@ -1638,13 +1602,16 @@ struct Engine {
           nt += popc32(m);
         }
         const unsigned mc = g.ballot(capped);
-        if (capped) {  // (cap, position) for the cap order
+        if (capped) {  // (cap, position) of the capped members
           const int slot = ncap + popc32(mc & g.lanemask_lt());
-          I.x_hi[slot] = dbits(smax(0.0, scap[p]));
+          const double cp = smax(0.0, scap[p]);
+          I.x_hi[slot] = dbits(cp);
           I.x_lo[slot] = (unsigned long long)p;
+          cmn = smin(cmn, cp);
         }
         ncap += popc32(mc);
       }
+      for (int m = G::N / 2; m > 0; m >>= 1) cmn = smin(cmn, g.shfl_xor(cmn, m));
       g.sync();
       {  // slot -> member incidence: extents from the counts, atomic fill
         int off = 0;
@@ -1671,17 +1638,14 @@ struct Engine {
         }
         g.sync();
       }
-      if (ncap > 1) sort_caps(ncap);  // caps ascending (cap >= 0: bit order)
       MF_TOC(OUT_CY_SUB + 1, q1);
       if (nt > s.max_touch) s.max_touch = nt;
       int nu = n;
-      int cptr = 0;
       double R = 0.0;
       while (nu > 0) {
         ++rounds;
         MF_TIC(q2);
-        while (cptr < ncap && frz[(int)I.x_lo[cptr]]) ++cptr;
-        const double cmin = cptr < ncap ? dsub(bits_to_d(I.x_hi[cptr]), R) : MF_INF;
+        const double cmin = ncap > 0 ? dsub(cmn, R) : MF_INF;
         double amin = MF_INF;
 #pragma unroll 4
         for (int jj = g.lane(); jj < nt; jj += G::N) {
@@ -1734,24 +1698,6 @@ struct Engine {
         g.sync();
         MF_TOC(OUT_CY_SUB + 3, q3);
         MF_TIC(q4);
-        int frozen = 0;
-        // cap freezes: the unfrozen prefix of the cap order with cap - eps <= R
-        for (; cptr < ncap; ++cptr) {
-          const int p = (int)I.x_lo[cptr];
-          if (frz[p]) continue;
-          const double cp = bits_to_d(I.x_hi[cptr]);
-          const double cap_eps = dmul(1e-12, smax(1.0, cp));
-          if (!(R >= dsub(cp, cap_eps))) break;
-          g.sync();
-          if (g.leader()) {
-            frz[p] = 1;
-            rate[p] = R;
-          }
-          const int rn = arnp[p];
-          for (int k = g.lane(); k < rn; k += G::N) g.atomic_add(&cnt[asl[p * RM + k]], -1);
-          g.sync();
-          ++frozen;
-        }
         // link freezes: every unfrozen member of every saturated slot, all in
         // one pass (a member on two saturated slots is claimed once)
         int got = 0;
@@ -1768,10 +1714,52 @@ struct Engine {
           }
         }
         g.sync();
-        if (ns > 0) {
+        // cap freezes (the same rate R, so the order against the link freezes
+        // is immaterial): drop frozen entries, freeze cap - eps <= R, and take
+        // the minimum cap of the survivors for the next round
+        if (ncap > 0) {
+          int nc2 = 0;
+          double mn = MF_INF;
+          for (int base = 0; base < ncap; base += G::N) {
+            const int i = base + g.lane();
+            bool keep = false, fz = false;
+            int p = 0;
+            double cp = 0.0;
+            if (i < ncap) {
+              p = (int)I.x_lo[i];
+              if (!frz[p]) {
+                cp = bits_to_d(I.x_hi[i]);
+                fz = R >= dsub(cp, dmul(1e-12, smax(1.0, cp)));
+                keep = !fz;
+              }
+            }
+            g.sync();  // every lane has read its entry before the in-place compaction
+            if (fz) {
+              frz[p] = 1;
+              rate[p] = R;
+              const int rn = arnp[p];
+              for (int k = 0; k < rn; ++k) g.atomic_add(&cnt[asl[p * RM + k]], -1);
+              ++got;
+            }
+            const unsigned mk = g.ballot(keep);
+            if (keep) {
+              const int slot = nc2 + popc32(mk & g.lanemask_lt());
+              I.x_hi[slot] = dbits(cp);
+              I.x_lo[slot] = (unsigned long long)p;
+              mn = smin(mn, cp);
+            }
+            nc2 += popc32(mk);
+          }
+          for (int m = G::N / 2; m > 0; m >>= 1) mn = smin(mn, g.shfl_xor(mn, m));
+          g.sync();
+          ncap = nc2;
+          cmn = mn;
+        }
+        int frozen = 0;
+        if (ns > 0 || has_caps) {
           int tot;
           g.excl_scan(got, &tot);
-          frozen += tot;
+          frozen = tot;
         }
         MF_TOC(OUT_CY_SUB + 4, q4);
         bytes += 32LL * nt + 24LL * frozen;

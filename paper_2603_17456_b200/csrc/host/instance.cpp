@@ -360,11 +360,20 @@ void derive_deadlines(Backend& be, const std::vector<InstanceInput*>& insts) {
     FairShareScheduler fs;
     fs.configure(fsp);
     fsp.horizon = 0.0 + 1e9;  // horizon reset, slack 1e9 (workload.cpp:189-191)
-    std::string pkey(reinterpret_cast<const char*>(&fsp), sizeof(fsp));
+    // key of the probe parameters, field by field (struct padding is not data)
+    static_assert(sizeof(InstParams) == 368, "new InstParams field: add it to the probe key");
+    std::string pkey;
+    auto put = [&pkey](auto v) { pkey.append(reinterpret_cast<const char*>(&v), sizeof(v)); };
+    put(fsp.policy), put(fsp.K);
+    for (double t : fsp.thr) put(t);
+    put(fsp.tick), put(fsp.horizon), put(fsp.livelock), put(fsp.max_batch_tokens), put(fsp.layers);
+    put(fsp.alpha), put(fsp.beta), put(fsp.kv), put(fsp.coll), put(fsp.units), put(fsp.hpu);
+    put(fsp.decode_hosts), put(fsp.prune_enable), put(fsp.drop_frac), put(fsp.workload_mode);
     probe_of[i].resize(in.reqs.size());
     for (size_t r = 0; r < in.reqs.size(); ++r) {
       const HostRequest& q = in.reqs[r];
-      const long bits = static_cast<long>(std::llround(q.reuse * 1e9));
+      long bits;  // the exact reuse fraction
+      std::memcpy(&bits, &q.reuse, sizeof(bits));
       auto key = std::make_tuple(static_cast<const void*>(in.topo.get()), pkey, q.tokens, bits, q.unit,
                                  q.source);
       auto it = cache.find(key);
