@@ -166,6 +166,7 @@ struct Sc {
   long long pruned;
   int max_active;
   int max_touch, max_pool;
+  double sat_max;  // 1e-12 * the largest link capacity: bounds every saturation threshold
   long long cy[32];
 };
 
@@ -1137,6 +1138,66 @@ struct Engine {
     return ncls;
   }
 
+  static constexpr int kMaxAdd = 64;  // merged into the previous order; more: full sort
+
+  // Order repair of the survivors ord[0, n1) of the previous step's order:
+  // while an adjacent pair is inverted (keys changed, e.g. SJF remaining
+  // sizes crossing), both elements of every inverted pair leave for the add
+  // list, appended after the n2 new flows at ord + n1. A displaced element is
+  // always part of a pair, so a few passes leave a sorted subsequence. False if
+  // the add list would exceed kMaxAdd.
+  MF_FN bool repair_order(int* ord, int* pn1, int* pn2) {
+    const int n1_0 = *pn1, n2 = *pn2;
+    int n1 = n1_0, nr = 0;
+    int* __restrict__ flg = I.x_aux;  // scratch outside the link bucketing
+    int* __restrict__ rb = I.y_aux;
+    for (;;) {
+      bool any = false;
+      for (int i = g.lane(); i < n1; i += G::N) {
+        const int v = ord[i];
+        const bool rm = (i > 0 && pos_less(v, ord[i - 1])) || (i + 1 < n1 && pos_less(ord[i + 1], v));
+        flg[i] = rm ? 1 : 0;
+        any = any || rm;
+      }
+      if (!g.any(any)) break;
+      g.sync();
+      int k = 0;
+      for (int base = 0; base < n1; base += G::N) {
+        const int i = base + g.lane();
+        const bool in = i < n1;
+        int v = 0;
+        bool rm = false;
+        if (in) {
+          v = ord[i];
+          rm = flg[i] != 0;
+        }
+        g.sync();  // every lane has read its entry before the in-place compaction
+        const unsigned mk = g.ballot(in && !rm);
+        if (in && !rm) ord[k + popc32(mk & g.lanemask_lt())] = v;
+        k += popc32(mk);
+        const unsigned mr = g.ballot(in && rm);
+        if (in && rm) rb[nr + popc32(mr & g.lanemask_lt())] = v;
+        nr += popc32(mr);
+      }
+      g.sync();
+      n1 = k;
+      if (nr + n2 > kMaxAdd) {  // give the survivors back (n1 + nr == n1_0) for a full sort
+        for (int i = g.lane(); i < nr; i += G::N) ord[n1 + i] = rb[i];
+        g.sync();
+        return false;
+      }
+    }
+    if (nr > 0) {  // add list = new flows, then the pulled survivors, at ord + n1
+      for (int i = g.lane(); i < n2; i += G::N) rb[nr + i] = ord[n1_0 + i];
+      g.sync();
+      for (int i = g.lane(); i < nr + n2; i += G::N) ord[n1 + i] = rb[i];
+      g.sync();
+    }
+    *pn1 = n1;
+    *pn2 = n2 + nr;
+    return true;
+  }
+
   // Sorted list of the active positions p with in_subset(p), written to ord.
   template <class P>
   MF_FN int sorted_subset(int* ord, P in_subset) {
@@ -1173,26 +1234,30 @@ struct Engine {
       n2 += popc32(m);
     }
     g.sync();
-    const int n = n1 + n2;
-    // still sorted? (keys may have changed since the last step)
-    bool broken = false;
-    for (int i = 1 + g.lane(); i < n1; i += G::N)
-      if (pos_less(ord[i], ord[i - 1])) broken = true;
-    if (g.any(broken) || n2 > 64) {
+    // keys may have changed since the last step: pull every adjacent inversion
+    // of the survivors into the add list; a full sort if that list grows large
+    if (n2 > kMaxAdd || !repair_order(ord, &n1, &n2)) {
+      const int n = n1 + n2;
       sort_ord(ord, n);
-    } else if (n2 > 0) {
-      // insertion sort of the few new flows, then a merge by ranks
-      if (g.leader()) {
-        for (int a = 1; a < n2; ++a) {
-          const int v = add[a];
-          int m = a;
-          while (m > 0 && pos_less(v, add[m - 1])) {
-            add[m] = add[m - 1];
-            --m;
-          }
-          add[m] = v;
-        }
+      for (int i = g.lane(); i < n; i += G::N) I.srt[i] = I.a_fid[ord[i]];
+      g.sync();
+      s.n_srt = n;
+      s.n_add = 0;
+      return n;
+    }
+    const int n = n1 + n2;
+    add = ord + n1;
+    if (n2 > 0) {
+      // rank sort of the few new flows (pos_less is a strict total order)
+      int* rb = I.y_aux;
+      for (int a = g.lane(); a < n2; a += G::N) {
+        const int v = add[a];
+        int rk = 0;
+        for (int b = 0; b < n2; ++b) rk += pos_less(add[b], v) ? 1 : 0;
+        rb[rk] = v;
       }
+      g.sync();
+      for (int a = g.lane(); a < n2; a += G::N) add[a] = rb[a];
       g.sync();
       int* tmp = I.s_ul;  // scratch (free outside allocate)
       for (int i = g.lane(); i < n; i += G::N) {
@@ -1459,7 +1524,8 @@ struct Engine {
             const int rn = arnp[p];
             for (int k = 0; k < rn; ++k) {
               const int l = arlp[p * RM + k];
-              if (res[l] <= dmul(1e-12, capv[l])) stop = true;
+              const double rl = res[l];
+              if (rl <= s.sat_max && rl <= dmul(1e-12, capv[l])) stop = true;
             }
             keep = !stop;
             if (stop)  // a frozen member leaves every link count for good
@@ -1514,7 +1580,7 @@ struct Engine {
     const unsigned short* __restrict__ slink = I.sl_link;
     const double* __restrict__ scap = I.s_cap;
     unsigned short* __restrict__ mem = I.c_mem;
-    uint8_t* __restrict__ frz = I.c_frz;
+    unsigned* __restrict__ frz = I.c_frz;  // member frozen bits, by active position
     if (kLinksOnChip) {
       MF_SH(res);
       MF_SH(cnt);
@@ -1522,6 +1588,7 @@ struct Engine {
       MF_SH(mend);
       MF_SH(tl);
       MF_SH(sat);
+      MF_SH(frz);
     }
     MF_TIC(q0);
     if (I.p.policy == POL_MFS) {  // rate-map insertion order (load_fraction)
@@ -1580,6 +1647,7 @@ struct Engine {
       MF_TIC(q1);
       int nt = 0, ncap = 0;
       double cmn = MF_INF;
+      for (int w = g.lane(); w < ((A + 31) >> 5); w += G::N) frz[w] = 0u;
       for (int base = 0; base < n; base += G::N) {
         const int i = base + g.lane();
         int p = 0, rn = 0;
@@ -1587,7 +1655,6 @@ struct Engine {
         if (i < n) {
           p = ord[o0 + i];
           rn = arnp[p];
-          frz[p] = 0;
           if (has_caps) capped = scap[p] < MF_INF;
         }
         for (int k = 0; k < RM; ++k) {
@@ -1683,7 +1750,9 @@ struct Engine {
             if (cn > 0) {
               const double r = dsub(res[j], dmul(inc, (double)cn));
               res[j] = r;
-              st = r <= dmul(1e-12, capv[slink[j]]);
+              // r <= 1e-12 * cap_j implies r <= sat_max (rounding is monotone):
+              // the capacity is loaded only for the rare candidates
+              st = r <= s.sat_max && r <= dmul(1e-12, capv[slink[j]]);
               live = !st;
             }
           }
@@ -1706,7 +1775,8 @@ struct Engine {
           const int e1 = mend[j];
           for (int e = mb[j] + g.lane(); e < e1; e += G::N) {
             const int p = mem[e];
-            if (frz[p] || g.atomic_exch_u8(&frz[p]) != 0) continue;
+            const unsigned bit = 1u << (p & 31);
+            if ((frz[p >> 5] & bit) || (g.atomic_or(&frz[p >> 5], bit) & bit)) continue;
             rate[p] = R;
             const int rn = arnp[p];
             for (int k = 0; k < rn; ++k) g.atomic_add(&cnt[asl[p * RM + k]], -1);
@@ -1727,7 +1797,7 @@ struct Engine {
             double cp = 0.0;
             if (i < ncap) {
               p = (int)I.x_lo[i];
-              if (!frz[p]) {
+              if (!(frz[p >> 5] & (1u << (p & 31)))) {
                 cp = bits_to_d(I.x_hi[i]);
                 fz = R >= dsub(cp, dmul(1e-12, smax(1.0, cp)));
                 keep = !fz;
@@ -1735,7 +1805,7 @@ struct Engine {
             }
             g.sync();  // every lane has read its entry before the in-place compaction
             if (fz) {
-              frz[p] = 1;
+              g.atomic_or(&frz[p >> 5], 1u << (p & 31));
               rate[p] = R;
               const int rn = arnp[p];
               for (int k = 0; k < rn; ++k) g.atomic_add(&cnt[asl[p * RM + k]], -1);
@@ -2784,7 +2854,13 @@ struct Engine {
     s.sl_hw = s.sl_nfree = s.n_unslotted = 0;
     s.rel_idx = false;
     for (int k = 0; k < 32; ++k) s.cy[k] = 0;
-    for (int l = g.lane(); l < I.nlinks; l += G::N) I.l2s[l] = 0xFFFFu;
+    double cmx = 0.0;
+    for (int l = g.lane(); l < I.nlinks; l += G::N) {
+      I.l2s[l] = 0xFFFFu;
+      cmx = smax(cmx, I.cap[l]);
+    }
+    for (int m = G::N / 2; m > 0; m >>= 1) cmx = smax(cmx, g.shfl_xor(cmx, m));
+    s.sat_max = dmul(1e-12, cmx);
     pool_copy(true, n_ev0);  // host-prepared initial events (manual mode)
     if (!I.host_init) {
       init_state();

@@ -28,6 +28,8 @@ struct SmemPlan {
 
 __host__ __device__ inline int align16(int x) { return (x + 15) & ~15; }
 
+constexpr int kFrzWords = 32;  // on-chip member frozen bits: active sets up to 1024 flows
+
 // Per-warp shared memory: the descriptor copy, the event pool, the link ->
 // slot map and the per-slot filling state. The active-flow arrays stay in
 // global memory (L1/L2): measured sweep instances reach 250-900 active flows,
@@ -40,6 +42,7 @@ __host__ inline SmemPlan make_plan(int nlinks) {
   int b = align16(sizeof(Inst));
   b += align16(p.ES * 8) * 2 + align16(p.ES * 4) * 3;
   b += align16(p.TS * 8) + 3 * align16(p.TS * 4) + 2 * align16(p.TS * 2);
+  b += align16(kFrzWords * 4);
   p.bytes = align16(b);
   return p;
 }
@@ -98,7 +101,7 @@ __global__ void __launch_bounds__(32)
       } else {
         q += 2 * align16(plan.ES * 8) + 3 * align16(plan.ES * 4);
       }
-      if (plan.TS > 0 && d->TS_cap > 0) {
+      if (plan.TS > 0 && d->TS_cap > 0 && d->A_cap <= 32 * kFrzWords) {
         // per-step slot state on chip; the slot bookkeeping stays in HBM
         // (its capacity bound must not change across suspend / resume)
         d->sl_res = reinterpret_cast<double*>(take(plan.TS * 8));
@@ -107,6 +110,7 @@ __global__ void __launch_bounds__(32)
         d->sl_end = reinterpret_cast<int*>(take(plan.TS * 4));
         d->sl_tl = reinterpret_cast<unsigned short*>(take(plan.TS * 2));
         d->sl_sat = reinterpret_cast<unsigned short*>(take(plan.TS * 2));
+        d->c_frz = reinterpret_cast<unsigned*>(take(kFrzWords * 4));
         slots_on_chip = true;
       }
     }

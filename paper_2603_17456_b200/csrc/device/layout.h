@@ -226,7 +226,7 @@ struct Inst {
   unsigned short* sl_tl;   // [TS] live slots of the class
   unsigned short* sl_sat;  // [TS] slots saturated this round
   unsigned short* c_mem;   // [A_cap * rmax] slot -> member incidence
-  uint8_t* c_frz;          // [A_cap] member frozen flags
+  unsigned* c_frz;         // [(A_cap+31)/32] member frozen bits
   unsigned short* s_tl;  // links touched by that class [nlinks]
   int* srt;         // sorted-subset order of the last decide (flow ids)
   int* srt_add;     // flows released since the last decide

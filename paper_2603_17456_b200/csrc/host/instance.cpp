@@ -723,7 +723,7 @@ void carve_instance(Carver& c, const InstanceInput& in, Inst& d, const Inst& top
   d.sl_tl = c.S<unsigned short>(nts);
   d.sl_sat = c.S<unsigned short>(nts);
   d.c_mem = c.S<unsigned short>(nA * d.rmax);
-  d.c_frz = c.S<uint8_t>(nA + 4);
+  d.c_frz = c.S<unsigned>((nA + 31) / 32);
   d.s_tl = c.S<unsigned short>(nl);
   d.srt = c.S<int>(nA);
   d.srt_add = c.S<int>(nA);
