@@ -946,6 +946,7 @@ struct Engine {
   }
   MF_FN void sort_ord(int* ord, int n) {
     if (n <= 1) return;
+    MF_TIC(o0);
     const int n2 = pow2ceil(n);
     for (int i = n + g.lane(); i < n2; i += G::N) ord[i] = -1;
     g.sync();
@@ -965,6 +966,7 @@ struct Engine {
         g.sync();
       }
     }
+    MF_TOC(OUT_CY_SUB + 13, o0);
   }
   // joint sort of x_hi/x_lo/x_val by (hi, lo)
   MF_FN void sort_x(int n) {
@@ -1087,7 +1089,9 @@ struct Engine {
     } else if (pol == POL_KARUNA) {  // baselines.cpp:92-135
       const int nd = compact(I.s_ord, [&](int p) { return has_dl(I.a_fid[p]); });
       if (nd > 0) {
+        MF_TIC(k0);
         karuna_caps(nd);
+        MF_TOC(OUT_CY_SUB + 11, k0);
         if (s.err) return 0;
         *has_caps = true;
         if (g.leader()) I.s_cls[0] = 0;
@@ -1201,6 +1205,13 @@ struct Engine {
   // Sorted list of the active positions p with in_subset(p), written to ord.
   template <class P>
   MF_FN int sorted_subset(int* ord, P in_subset) {
+    MF_TIC(z0);
+    const int n = sorted_subset_(ord, in_subset);
+    MF_TOC(OUT_CY_SUB + 12, z0);
+    return n;
+  }
+  template <class P>
+  MF_FN int sorted_subset_(int* ord, P in_subset) {
     if (s.n_add < 0) {  // add list overflowed: sort every member from scratch
       const int n = compact(ord, in_subset);
       sort_ord(ord, n);

@@ -1,5 +1,7 @@
 #include "instance.hpp"
 
+#include <mutex>
+
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
@@ -294,10 +296,36 @@ std::shared_ptr<TopoImage> build_topo_image(const Fabric& f, const Layout& lay) 
   return t;
 }
 
+// Topology images are immutable once built; the instances of a sweep share
+// one per distinct (fabric, layout) key text instead of rebuilding the fabric
+// and its routes. A miss validates in the reference order (fabric, layout).
+std::shared_ptr<TopoImage> shared_topo_image(const Config& cfg) {
+  std::string key;
+  for (const char* k : {"topology.kind", "topology.hosts", "topology.nics_per_host",
+                        "topology.link_bytes_per_s", "topology.link_gbps", "cluster.prefill_units",
+                        "cluster.hosts_per_unit", "cluster.decode_hosts"})
+    key += (cfg.has(k) ? "=" + cfg.str(k, "") : std::string("-")) + '\x1f';
+  static std::mutex mu;
+  static std::map<std::string, std::weak_ptr<TopoImage>> cache;
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = cache.find(key);
+    if (it != cache.end())
+      if (auto t = it->second.lock()) return t;
+  }
+  const Fabric fab = Fabric::from(cfg);
+  const Layout lay = Layout::from(cfg);
+  auto t = build_topo_image(fab, lay);
+  t->hosts = fab.hosts();
+  std::lock_guard<std::mutex> lock(mu);
+  cache[key] = t;
+  return t;
+}
+
 InstanceInput workload_instance(const Config& cfg) {
   InstanceInput in;
   const PolicyKind kind = parse_policy(cfg.str("policy", "fs"));
-  const Fabric fab = Fabric::from(cfg);
+  in.topo = shared_topo_image(cfg);
   const Layout lay = Layout::from(cfg);
   const CostModel cost = CostModel::from(cfg);
   const RunParams rp = RunParams::from(cfg);
@@ -308,10 +336,10 @@ InstanceInput workload_instance(const Config& cfg) {
     in.reqs = read_trace(spec.trace, lay, cost);
   auto sched = make_scheduler(kind, cfg);
   sched->configure(in.p);
-  if (lay.total_hosts() > fab.hosts())
+  if (lay.total_hosts() > in.topo->hosts)
     throw ConfigError("config key 'cluster.prefill_units': layout needs " +
                       std::to_string(lay.total_hosts()) + " hosts, topology has " +
-                      std::to_string(fab.hosts()));
+                      std::to_string(in.topo->hosts));
   double last = 0.0;
   for (HostRequest& r : in.reqs) {
     if (r.tokens > rp.max_batch_tokens)
@@ -325,7 +353,6 @@ InstanceInput workload_instance(const Config& cfg) {
       throw WorkloadError("request: reuse_fraction > 0 needs a reuse_source");
     last = std::max(last, r.arrival);
   }
-  in.topo = build_topo_image(fab, lay);
   in.policy = sched->name();
   in.seed = static_cast<long>(spec.seed);
   in.rate = spec.rate;

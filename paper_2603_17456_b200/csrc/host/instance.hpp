@@ -63,7 +63,7 @@ struct TopoImage {
   RouteTable routes;
   std::vector<int> rt_reuse, rt_p2d, rt_coll;
   int lr_cap = 1;  // max distinct links one request's load touches
-  size_t dev_off = 0;
+  int hosts = 0;   // hosts of the fabric
 };
 std::shared_ptr<TopoImage> build_topo_image(const Fabric& f, const Layout& lay);
 

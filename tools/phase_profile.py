@@ -16,6 +16,6 @@ for pol in (sys.argv[2] if len(sys.argv) > 2 else "fs,sjf,edf,karuna,mfs").split
     cyc = c[16:24]
     print(f"{pol}: maxA {c[8]} events {ev} steps {st} kernel {ms:.0f} ms = {1e6*ms/1e3/ev:.1f} us/ev; cycles/event: " +
           " ".join(f"{n}={v/ev:.0f}" for n, v in zip(names, cyc)) + f" total={cyc.sum()/ev:.0f}", flush=True)
-    sub = c[24:35]
-    sn = ["a_prep", "a_count", "a_inc", "a_apply", "a_freeze", "a_restore", "finish", "release", "compute", "depart", "admit"]
+    sub = c[24:38]
+    sn = ["a_prep", "a_count", "a_inc", "a_apply", "a_freeze", "a_restore", "finish", "release", "compute", "depart", "admit", "k_caps", "subset", "fullsort"]
     print("    sub cycles/event: " + " ".join(f"{n}={v/ev:.0f}" for n, v in zip(sn, sub)), f"rounds/step={c[13]/st:.1f}", flush=True)
