@@ -192,15 +192,18 @@ MF_FN bool ev_less(const Ev& x, const Ev& y) {
   return x.seq < y.seq;
 }
 
-// kLinksOnChip: the link -> slot map and the per-slot filling state were
-// staged in shared memory by the kernel (see engine_kernel.cu make_plan).
-template <class G, bool kOnChip = false, bool kLinksOnChip = false>
+// One engine per warp. `chip`: the kernel staged the per-slot filling state
+// and the frozen-member bits in shared memory (engine_kernel.cu make_plan);
+// only the filling rounds are specialised on it, the rest of the engine is
+// one copy of code (instruction-cache footprint).
+template <class G>
 struct Engine {
   G g;
   Inst& I;  // per-warp copy (shared memory on the device), arrays possibly re-pointed
+  const bool chip;
   Sc s;
 
-  MF_FN explicit Engine(Inst& inst) : I(inst) {}
+  MF_FN explicit Engine(Inst& inst, bool on_chip = false) : I(inst), chip(on_chip) {}
 
   // ----------------------------------------------------------------- util
   template <class T>
@@ -944,7 +947,7 @@ struct Engine {
     return I.s_k0[pa] == I.s_k0[pb] && I.s_k1[pa] == I.s_k1[pb] && I.s_k2[pa] == I.s_k2[pb] &&
            I.s_k3[pa] == I.s_k3[pb];
   }
-  MF_FN void sort_ord(int* ord, int n) {
+  MF_NOINLINE void sort_ord(int* ord, int n) {
     if (n <= 1) return;
     MF_TIC(o0);
     const int n2 = pow2ceil(n);
@@ -1005,7 +1008,7 @@ struct Engine {
   }
 
   // group s_ord[o0, o0+n) into classes of equal keys, appending to s_cls
-  MF_FN int group_classes(int o0, int n, int ncls) {
+  MF_NOINLINE int group_classes(int o0, int n, int ncls) {
     for (int base = 0; base < n; base += G::N) {
       int i = base + g.lane();
       int h = 0;
@@ -1019,13 +1022,18 @@ struct Engine {
     return ncls;
   }
 
-  // compact active positions satisfying pred (in active order) into ord
-  template <class P>
-  MF_FN int compact(int* ord, P pred) {
+  // flow subsets of the policy orders: all active flows, those with / without a deadline
+  enum { SUB_ALL = 0, SUB_DL = 1, SUB_NODL = 2 };
+  MF_FN bool in_sub(int p, int mode) const {
+    return mode == SUB_ALL || (has_dl(I.a_fid[p]) == (mode == SUB_DL));
+  }
+
+  // compact active positions of a subset (in active order) into ord
+  MF_NOINLINE int compact(int* ord, int mode) {
     int n = 0;
     for (int base = 0; base < s.n_active; base += G::N) {
       int p = base + g.lane();
-      int c = (p < s.n_active && pred(p)) ? 1 : 0;
+      int c = (p < s.n_active && in_sub(p, mode)) ? 1 : 0;
       int tot;
       int off = g.excl_scan(c, &tot);
       if (c) ord[n + off] = p;
@@ -1067,7 +1075,7 @@ struct Engine {
         I.s_k3[p] = 0;
       }
       g.sync();
-      const int n = sorted_subset(I.s_ord, [&](int) { return true; });
+      const int n = sorted_subset(I.s_ord, SUB_ALL);
       ncls = group_classes(0, n, 0);
     } else if (pol == POL_EDF) {  // baselines.cpp:59-90
       for (int p = g.lane(); p < A; p += G::N) {
@@ -1078,16 +1086,16 @@ struct Engine {
         I.s_k3[p] = 0;
       }
       g.sync();
-      const int ne = sorted_subset(I.s_ord, [&](int p) { return has_dl(I.a_fid[p]); });
+      const int ne = sorted_subset(I.s_ord, SUB_DL);
       ncls = group_classes(0, ne, 0);
-      const int ni = compact(I.s_ord + ne, [&](int p) { return !has_dl(I.a_fid[p]); });
+      const int ni = compact(I.s_ord + ne, SUB_NODL);
       if (ni > 0) {
         if (g.leader()) I.s_cls[ncls] = ne;
         g.sync();
         ++ncls;
       }
     } else if (pol == POL_KARUNA) {  // baselines.cpp:92-135
-      const int nd = compact(I.s_ord, [&](int p) { return has_dl(I.a_fid[p]); });
+      const int nd = compact(I.s_ord, SUB_DL);
       if (nd > 0) {
         MF_TIC(k0);
         karuna_caps(nd);
@@ -1105,7 +1113,7 @@ struct Engine {
         I.s_k3[p] = 0;
       }
       g.sync();
-      const int nr = sorted_subset(I.s_ord + nd, [&](int p) { return !has_dl(I.a_fid[p]); });
+      const int nr = sorted_subset(I.s_ord + nd, SUB_NODL);
       ncls = group_classes(nd, nr, ncls);
     } else {  // MFS arbitrate (rmlq.cpp:201-260)
       for (int p = g.lane(); p < A; p += G::N) {
@@ -1133,7 +1141,7 @@ struct Engine {
         I.s_k3[p] = dord(k3);
       }
       g.sync();
-      const int n = sorted_subset(I.s_ord, [&](int) { return true; });
+      const int n = sorted_subset(I.s_ord, SUB_ALL);
       ncls = group_classes(0, n, 0);
     }
     if (g.leader()) I.s_cls[ncls] = A;
@@ -1150,7 +1158,7 @@ struct Engine {
   // list, appended after the n2 new flows at ord + n1. A displaced element is
   // always part of a pair, so a few passes leave a sorted subsequence. False if
   // the add list would exceed kMaxAdd.
-  MF_FN bool repair_order(int* ord, int* pn1, int* pn2) {
+  MF_NOINLINE bool repair_order(int* ord, int* pn1, int* pn2) {
     const int n1_0 = *pn1, n2 = *pn2;
     int n1 = n1_0, nr = 0;
     int* __restrict__ flg = I.x_aux;  // scratch outside the link bucketing
@@ -1202,18 +1210,16 @@ struct Engine {
     return true;
   }
 
-  // Sorted list of the active positions p with in_subset(p), written to ord.
-  template <class P>
-  MF_FN int sorted_subset(int* ord, P in_subset) {
+  // Sorted list of the active positions p with in_sub(p, mode), written to ord.
+  MF_NOINLINE int sorted_subset(int* ord, int mode) {
     MF_TIC(z0);
-    const int n = sorted_subset_(ord, in_subset);
+    const int n = sorted_subset_(ord, mode);
     MF_TOC(OUT_CY_SUB + 12, z0);
     return n;
   }
-  template <class P>
-  MF_FN int sorted_subset_(int* ord, P in_subset) {
+  MF_FN int sorted_subset_(int* ord, int mode) {
     if (s.n_add < 0) {  // add list overflowed: sort every member from scratch
-      const int n = compact(ord, in_subset);
+      const int n = compact(ord, mode);
       sort_ord(ord, n);
       for (int i = g.lane(); i < n; i += G::N) I.srt[i] = I.a_fid[ord[i]];
       g.sync();
@@ -1227,7 +1233,7 @@ struct Engine {
       const int i = base + g.lane();
       int p = -1;
       if (i < s.n_srt) p = I.f_apos[I.srt[i]];
-      const bool keep = p >= 0 && in_subset(p);
+      const bool keep = p >= 0 && in_sub(p, mode);
       const unsigned m = g.ballot(keep);
       if (keep) ord[n1 + popc32(m & ((1u << g.lane()) - 1u))] = p;
       n1 += popc32(m);
@@ -1239,7 +1245,7 @@ struct Engine {
       const int i = base + g.lane();
       int p = -1;
       if (i < s.n_add) p = I.f_apos[I.srt_add[i]];
-      const bool keep = p >= 0 && in_subset(p);
+      const bool keep = p >= 0 && in_sub(p, mode);
       const unsigned m = g.ballot(keep);
       if (keep) add[n2 + popc32(m & ((1u << g.lane()) - 1u))] = p;
       n2 += popc32(m);
@@ -1377,10 +1383,14 @@ struct Engine {
   // freeze permanently), which equals the reference's per-round recount; the
   // rounds then touch only that class's links and its unfrozen members.
   MF_FN void allocate(int ncls, bool has_caps) {
-    if (I.TS_cap > 0 && s.n_unslotted == 0)
-      allocate_slots(ncls, has_caps);
-    else
+    if (I.TS_cap > 0 && s.n_unslotted == 0) {
+      if (chip)
+        allocate_slots<true>(ncls, has_caps);
+      else
+        allocate_slots<false>(ncls, has_caps);
+    } else {
       allocate_generic(ncls, has_caps);
+    }
   }
 
   // per-member rounds over global-memory arrays (instances beyond the
@@ -1572,6 +1582,7 @@ struct Engine {
   }
 
   // class filling with the shared class rate over the link slots
+  template <bool kLinksOnChip>
   MF_NOINLINE void allocate_slots(int ncls, bool has_caps) {
     const int A = s.n_active;
     const int RM = I.rmax;

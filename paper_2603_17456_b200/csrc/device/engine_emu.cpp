@@ -32,7 +32,7 @@ class EmuBackend final : public Backend {
               long long) override {
     for (int i = 0; i < n; ++i) {
       mfb::Inst local = d[i];
-      mfb::Engine<mfb::SerialLanes, false, false> eng(local);
+      mfb::Engine<mfb::SerialLanes> eng(local);
       if (eng.run(budget)) --remaining_;
     }
     ++launches_;

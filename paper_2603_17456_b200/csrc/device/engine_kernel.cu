@@ -47,10 +47,20 @@ __host__ inline SmemPlan make_plan(int nlinks) {
   return p;
 }
 
+__device__ __forceinline__ int sm_id() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+  return (int)r;
+}
+
+// order[0, n): instance ids in claim groups (one per policy), estimated work
+// descending within a group; order[n + g] = offset of group g. A warp claims
+// from its SM's home group first -- SMs are mapped onto the groups in
+// proportion to their sizes -- then from the others.
 __global__ void __launch_bounds__(32)
     mfsim_engine_kernel(const Inst* __restrict__ insts, const int* __restrict__ order, int n,
-                        int* __restrict__ next, SmemPlan plan, long long budget,
-                        long long slice_ns, int* __restrict__ remaining) {
+                        int groups, int nsm, int* __restrict__ next, SmemPlan plan,
+                        long long budget, long long slice_ns, int* __restrict__ remaining) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31;
   Inst* d = reinterpret_cast<Inst*>(smem);
@@ -62,12 +72,23 @@ __global__ void __launch_bounds__(32)
     __syncwarp();
     deadline = t0 + (unsigned long long)slice_ns;
   }
+  const int* __restrict__ goff = order + n;
+  int home = 0;
+  {
+    const long long pos = (long long)sm_id() * n / nsm;
+    while (home + 1 < groups && goff[home + 1] <= pos) ++home;
+  }
   for (;;) {
-    int i = 0;
-    if (lane == 0) i = atomicAdd(next, 1);
+    int i = -1;
+    if (lane == 0) {
+      for (int k = 0; k < groups && i < 0; ++k) {
+        const int gi = (home + k) % groups;
+        const int c = atomicAdd(&next[gi], 1);
+        if (goff[gi] + c < goff[gi + 1]) i = order[goff[gi] + c];
+      }
+    }
     i = __shfl_sync(0xffffffffu, i, 0);
-    if (i >= n) return;
-    i = order[i];  // longest estimated instances first
+    if (i < 0) return;
     {  // descriptor copy (8-byte words across the warp)
       const unsigned long long* src = reinterpret_cast<const unsigned long long*>(insts + i);
       unsigned long long* dst = reinterpret_cast<unsigned long long*>(d);
@@ -116,14 +137,8 @@ __global__ void __launch_bounds__(32)
     }
     slots_on_chip = __shfl_sync(0xffffffffu, slots_on_chip, 0);
     __syncwarp();
-    bool done;
-    if (slots_on_chip) {
-      Engine<WarpLanes, false, true> eng(*d);
-      done = eng.run(budget, deadline);
-    } else {
-      Engine<WarpLanes, false, false> eng(*d);
-      done = eng.run(budget, deadline);
-    }
+    Engine<WarpLanes> eng(*d, slots_on_chip);
+    const bool done = eng.run(budget, deadline);
     if (done && lane == 0) atomicSub(remaining, 1);
     __syncwarp();
   }
@@ -147,7 +162,7 @@ class CudaBackend final : public Backend {
     stream_ = own_;
     ck(cudaEventCreate(&e0_), "cudaEventCreate");
     ck(cudaEventCreate(&e1_), "cudaEventCreate");
-    ck(cudaMalloc(&counter_, 2 * sizeof(int)), "cudaMalloc counter");
+    ck(cudaMalloc(&counter_, (1 + kMaxGroups) * sizeof(int)), "cudaMalloc counter");
     ck(cudaMallocHost(&remain_host_, sizeof(int)), "cudaMallocHost");
     ck(cudaDeviceGetAttribute(&sms_, cudaDevAttrMultiProcessorCount, device), "attr");
     ck(cudaFuncSetAttribute(mfb::mfsim_engine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -192,10 +207,10 @@ class CudaBackend final : public Backend {
     if (per_sm < 1) per_sm = 1;
     int grid = sms_ * per_sm;
     if (n < grid) grid = n > 0 ? n : 1;
-    ck(cudaMemsetAsync(counter_, 0, sizeof(int), stream_), "memset");
+    ck(cudaMemsetAsync(counter_ + 1, 0, sizeof(int) * kMaxGroups, stream_), "memset");
     ck(cudaEventRecord(e0_, stream_), "event");
-    mfb::mfsim_engine_kernel<<<grid, 32, plan.bytes, stream_>>>(d, order, n, counter_, plan,
-                                                                budget, slice_ns, counter_ + 1);
+    mfb::mfsim_engine_kernel<<<grid, 32, plan.bytes, stream_>>>(
+        d, order, n, hint.groups, sms_, counter_ + 1, plan, budget, slice_ns, counter_);
     ck(cudaGetLastError(), "launch");
     ck(cudaEventRecord(e1_, stream_), "event");
     ++launches_;
@@ -205,12 +220,12 @@ class CudaBackend final : public Backend {
   // instances not yet finished (a fresh batch sets it to n)
   void set_remaining(int n) override {
     *remain_host_ = n;
-    ck(cudaMemcpyAsync(counter_ + 1, remain_host_, sizeof(int), cudaMemcpyHostToDevice, stream_),
+    ck(cudaMemcpyAsync(counter_, remain_host_, sizeof(int), cudaMemcpyHostToDevice, stream_),
        "remaining");
     ck(cudaStreamSynchronize(stream_), "remaining");
   }
   int remaining() override {
-    ck(cudaMemcpyAsync(remain_host_, counter_ + 1, sizeof(int), cudaMemcpyDeviceToHost, stream_),
+    ck(cudaMemcpyAsync(remain_host_, counter_, sizeof(int), cudaMemcpyDeviceToHost, stream_),
        "remaining");
     ck(cudaStreamSynchronize(stream_), "remaining");
     return *remain_host_;

@@ -955,7 +955,7 @@ void Batch::pack() {
       st_dev_ = static_cast<char*>(be_.dev_alloc(st_bytes_ + 64));
       out_dev_ = static_cast<char*>(be_.dev_alloc(out_bytes_ + 64));
       desc_dev_ = static_cast<Inst*>(be_.dev_alloc(sizeof(Inst) * std::max(n, 1)));
-      order_dev_ = static_cast<int*>(be_.dev_alloc(sizeof(int) * std::max(n, 1)));
+      order_dev_ = static_cast<int*>(be_.dev_alloc(sizeof(int) * (n + kMaxGroups + 1)));
       phase_dev_ = static_cast<int*>(be_.dev_alloc(sizeof(int) * std::max(n, 1)));
     }
   }
@@ -969,9 +969,21 @@ void Batch::pack() {
     const int pol = d.p.policy >= 0 && d.p.policy < 5 ? d.p.policy : 0;
     cost[i] = factor[pol] * (double(d.F_cap) + 2.0 * d.n_req);
   }
+  // claim groups: one per policy, so that the warps sharing an SM run the same
+  // policy's code (the engine's instruction footprint exceeds the i-cache)
   order_.resize(n);
   std::iota(order_.begin(), order_.end(), 0);
-  std::stable_sort(order_.begin(), order_.end(), [&](int a, int b) { return cost[a] > cost[b]; });
+  std::stable_sort(order_.begin(), order_.end(), [&](int a, int b) {
+    if (desc_[a].p.policy != desc_[b].p.policy) return desc_[a].p.policy < desc_[b].p.policy;
+    return cost[a] > cost[b];
+  });
+  std::vector<int> off{0};
+  for (int k = 1; k < n; ++k)
+    if (desc_[order_[k]].p.policy != desc_[order_[k - 1]].p.policy) off.push_back(k);
+  off.push_back(n);
+  hint_.groups = static_cast<int>(off.size()) - 1;
+  if (hint_.groups > kMaxGroups) throw InternalError("more claim groups than the kernel supports");
+  order_.insert(order_.end(), off.begin(), off.end());
 }
 
 void Batch::upload_inputs() { be_.h2d(in_dev_, in_host_, in_bytes_); }

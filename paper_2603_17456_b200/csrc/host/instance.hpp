@@ -31,7 +31,9 @@ constexpr int kSmemSlots = 256;       // per-slot filling state staged on chip
 struct LaunchHint {
   int rmax = 1;    // longest route of any instance
   int nlinks = 1;  // most links of any instance
+  int groups = 1;  // claim groups (one per policy): order[n .. n+groups] holds their offsets
 };
+constexpr int kMaxGroups = 8;
 
 // Device execution backend: the product build links the CUDA backend only.
 class Backend {
@@ -44,7 +46,8 @@ class Backend {
   virtual void host_free(void* p) = 0;
   virtual void h2d(void* dst, const void* src, size_t n) = 0;  // stream-ordered
   virtual void d2h(void* dst, const void* src, size_t n) = 0;
-  // order: device array, a permutation of [0, n) giving the claim order;
+  // order: device array, a permutation of [0, n) giving the claim order, in
+  // hint.groups contiguous groups whose offsets follow at order[n..n+groups];
   // budget: events per instance in this launch (<= 0: run to completion)
   virtual void launch(const mfb::Inst* d_insts, const int* order, int n, const LaunchHint& hint,
                       long long budget, long long slice_ns) = 0;
