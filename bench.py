@@ -35,6 +35,18 @@ sys.path.insert(0, HERE)
 
 PEAKS = os.path.join(HERE, "MEASURED_PEAKS.json")
 HBM_FALLBACK = 6650.0
+NCU_SUMMARY = os.path.join(HERE, "profiles", "r01_ncu_engine_summary.json")
+
+
+def ncu_traffic(events_per_launch: float):
+    """DRAM bytes per launch of the engine kernel from the committed ncu --set full
+    capture (dram__bytes_read.sum + dram__bytes_write.sum), scaled from the
+    captured launch to this run's launch by simulated events (bytes per event)."""
+    try:
+        s = json.load(open(NCU_SUMMARY))
+        return s["dram_bytes_per_event"] * events_per_launch, os.path.relpath(NCU_SUMMARY, HERE)
+    except Exception:
+        return None, None
 
 
 def parse():
@@ -302,6 +314,7 @@ def main():
     e2e = e2e_events / e2e_s
     kernel_ms = dev_ms / args.steps
     achieved = algo_bytes / (dev_ms / 1000.0) / 1e9  # rank 0's launches
+    traffic, traffic_src = ncu_traffic(events / world / args.steps)
     try:
         peaks = json.load(open(PEAKS))
         peak, peak_src = float(peaks["hbm_gbs"]), "measured"
@@ -319,8 +332,10 @@ def main():
                     "d2h_bytes_per_step": int(d2h)},
             "gpu_launches": args.steps,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
-                         "kernel": "mfsim_engine_kernel"},
+                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                         "kernel": "mfsim_engine_kernel",
+                         "algo_bytes_per_launch": algo_bytes / args.steps,
+                         "traffic_source": traffic_src},
             "clocks": clk.summary(),
             "events_per_step": events / args.steps,
             "setup_s_rank0": setup_s,
