@@ -271,7 +271,9 @@ static void fab_star(fabric* f, int hosts, double c) { /* topology.cpp:98-106 */
   for (int h = 0; h < hosts; ++h) fab_duplex(f, h, hosts, c);
   f->hosts = hosts;
 }
-static void fab_fattree(fabric* f, int hosts, double c) { /* topology.cpp:108-145 */
+static void fab_fattree(fabric* f, int hosts, double c, double os) { /* topology.cpp:108-145 */
+  /* extension: switch-to-switch links carry c / os (os = topology.oversubscription) */
+  double u = os == 1.0 ? c : c / os;
   int k = 2;
   while (k * k * k / 4 < hosts) k += 2;
   int half = k / 2;
@@ -289,10 +291,10 @@ static void fab_fattree(fabric* f, int hosts, double c) { /* topology.cpp:108-14
   }
   for (int p = 0; p < k; ++p)
     for (int e = 0; e < half; ++e)
-      for (int a = 0; a < half; ++a) fab_duplex(f, EDGE(p, e), AGG(p, a), c);
+      for (int a = 0; a < half; ++a) fab_duplex(f, EDGE(p, e), AGG(p, a), u);
   for (int p = 0; p < k; ++p)
     for (int a = 0; a < half; ++a)
-      for (int cc = a * half; cc < (a + 1) * half; ++cc) fab_duplex(f, AGG(p, a), CORE(cc), c);
+      for (int cc = a * half; cc < (a + 1) * half; ++cc) fab_duplex(f, AGG(p, a), CORE(cc), u);
   f->hosts = hosts;
 }
 
@@ -1909,8 +1911,12 @@ static void build_fabric(const kvcfg* c, fabric* F) {
   double cap = cfg_raw(c, "topology.link_bytes_per_s")
                    ? cfg_num(c, "topology.link_bytes_per_s", 0) * (double)nics
                    : cfg_num(c, "topology.link_gbps", 1.0) * 1e9 / 8.0 * (double)nics;
-  if (!strcmp(kind, "star")) fab_star(F, (int)hosts, cap);
-  else if (!strcmp(kind, "fattree")) fab_fattree(F, (int)hosts, cap);
+  double os = cfg_num(c, "topology.oversubscription", 1.0);
+  if (!(os >= 1.0) || os == INF) fail(2, "config: topology.oversubscription must be >= 1");
+  if (!strcmp(kind, "star")) {
+    if (os != 1.0) fail(2, "config: oversubscription needs a fat-tree");
+    fab_star(F, (int)hosts, cap);
+  } else if (!strcmp(kind, "fattree")) fab_fattree(F, (int)hosts, cap, os);
   else fail(2, "config: unknown topology");
   fab_finish(F);
 }

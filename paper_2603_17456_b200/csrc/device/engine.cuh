@@ -288,7 +288,7 @@ struct Engine {
         bsi = (2 << 28) | i;
       }
     }
-#pragma unroll 4
+MF_UNROLL
     for (int p = g.lane(); p < na; p += G::N) {
       const unsigned long long k = as[p];
       const double t = at[p];
@@ -298,16 +298,7 @@ struct Engine {
         bsi = (3 << 28) | p;
       }
     }
-    for (int m = G::N / 2; m > 0; m >>= 1) {
-      const double ot = g.shfl_xor(bt, m);
-      const unsigned long long ok = g.shfl_xor(bk, m);
-      const int os = g.shfl_xor(bsi, m);
-      if (ot < bt || (ot == bt && ok < bk)) {
-        bt = ot;
-        bk = ok;
-        bsi = os;
-      }
-    }
+    g.argmin_tk(&bt, &bk, &bsi);  // event times are >= 0 (or -0), never NaN
     Ev best;
     best.t = bt;
     best.klass = (int)(bk >> 61);
@@ -394,7 +385,7 @@ struct Engine {
       double* __restrict__ rem = I.a_rem;
       const double* __restrict__ rt = I.a_rate;
       bool bad = false;
-#pragma unroll 4
+MF_UNROLL
       for (int p = g.lane(); p < na; p += G::N) {
         double x = dsub(rem[p], dmul(rt[p], dt));
         if (x < 0.0) {
@@ -1353,7 +1344,7 @@ struct Engine {
       int e0, e1;
       const int l = bucket_at(j, &e0, &e1);
       double dmd = 0.0;
-#pragma unroll 4
+MF_UNROLL
       for (int a = e0; a < e1; ++a) dmd = dadd(dmd, I.y_val[a]);
       I.l_x[l] = dmd;
     }
@@ -1436,7 +1427,7 @@ struct Engine {
         }
         double mine = MF_INF;
         for (int k = g.lane(); k < rn; k += G::N) mine = smin(mine, smax(0.0, res[arlp[p * RM + k]]));
-        for (int m = G::N / 2; m > 0; m >>= 1) mine = smin(mine, g.shfl_xor(mine, m));
+        mine = g.min_nonneg(mine);  // smax(0, residual) >= 0
         r = smin(r, mine);
         g.sync();
         for (int k = g.lane(); k < rn; k += G::N) {
@@ -1481,7 +1472,7 @@ struct Engine {
         // whose exact quotient can be the minimum lies within that margin of
         // the approximate minimum; only those are divided exactly.
         double amin = MF_INF;
-#pragma unroll 4
+MF_UNROLL
         for (int j = g.lane(); j < nt; j += G::N) {
           const int l = tl[j];
           const int cn = cnt[l];
@@ -1490,36 +1481,35 @@ struct Engine {
         }
         double cmin = MF_INF;
         if (has_caps) {
-#pragma unroll 4
+MF_UNROLL
           for (int i = g.lane(); i < nu; i += G::N) {
             const int p = ul[i];
             const double cp = scap[p];
             if (cp < MF_INF) cmin = smin(cmin, dsub(smax(0.0, cp), rate[p]));
           }
         }
-        for (int m = G::N / 2; m > 0; m >>= 1) {
-          amin = smin(amin, g.shfl_xor(amin, m));
-          cmin = smin(cmin, g.shfl_xor(cmin, m));
-        }
+        amin = g.min_nonneg(amin);
+        for (int m = G::N / 2; m > 0; m >>= 1) cmin = smin(cmin, g.shfl_xor(cmin, m));
         const double athr = dadd(amin, dmul(amin, 0x1p-44));
         double inc = cmin;
         if (amin <= cmin) {  // a link share may be the minimum: exact quotients near it
-#pragma unroll 4
+          double q = MF_INF;
+MF_UNROLL
           for (int j = g.lane(); j < nt; j += G::N) {
             const int l = tl[j];
             const int cn = cnt[l];
             const double r = smax(0.0, res[l]);
-            if (cn > 0 && dmul(r, recip(cn)) <= athr) inc = smin(inc, ddiv(r, (double)cn));
+            if (cn > 0 && dmul(r, recip(cn)) <= athr) q = smin(q, ddiv(r, (double)cn));
           }
-          for (int m = G::N / 2; m > 0; m >>= 1) inc = smin(inc, g.shfl_xor(inc, m));
+          inc = smin(inc, g.min_nonneg(q));  // as in allocate_slots
         }
         inc = smax(inc, 0.0);
-#pragma unroll 4
+MF_UNROLL
         for (int i = g.lane(); i < nu; i += G::N) {
           const int p = ul[i];
           rate[p] = dadd(rate[p], inc);
         }
-#pragma unroll 4
+MF_UNROLL
         for (int j = g.lane(); j < nt; j += G::N) {
           const int l = tl[j];
           const int cn = cnt[l];
@@ -1645,7 +1635,7 @@ struct Engine {
         }
         double mine = MF_INF;
         for (int k = g.lane(); k < rn; k += G::N) mine = smin(mine, smax(0.0, res[asl[p * RM + k]]));
-        for (int m = G::N / 2; m > 0; m >>= 1) mine = smin(mine, g.shfl_xor(mine, m));
+        mine = g.min_nonneg(mine);  // smax(0, residual) >= 0
         r = smin(r, mine);
         g.sync();
         for (int k = g.lane(); k < rn; k += G::N) {
@@ -1700,7 +1690,7 @@ struct Engine {
         }
         ncap += popc32(mc);
       }
-      for (int m = G::N / 2; m > 0; m >>= 1) cmn = smin(cmn, g.shfl_xor(cmn, m));
+      cmn = g.min_nonneg(cmn);  // smax(0, cap) >= 0
       g.sync();
       {  // slot -> member incidence: extents from the counts, atomic fill
         int off = 0;
@@ -1736,25 +1726,27 @@ struct Engine {
         MF_TIC(q2);
         const double cmin = ncap > 0 ? dsub(cmn, R) : MF_INF;
         double amin = MF_INF;
-#pragma unroll 4
+MF_UNROLL
         for (int jj = g.lane(); jj < nt; jj += G::N) {
           const int j = tl[jj];
           const int cn = cnt[j];
           const double r = res[j];
           if (cn > 0) amin = smin(amin, dmul(smax(0.0, r), frecip(cn)));
         }
-        for (int m = G::N / 2; m > 0; m >>= 1) amin = smin(amin, g.shfl_xor(amin, m));
+        amin = g.min_nonneg(amin);  // smax(0, r) / cnt >= 0
         double inc = cmin;
         if (amin <= cmin) {  // exact quotients only within the approximation margin
           const double athr = dadd(amin, dmul(amin, 0x1p-18));
-#pragma unroll 4
+          double q = MF_INF;
+MF_UNROLL
           for (int jj = g.lane(); jj < nt; jj += G::N) {
             const int j = tl[jj];
             const int cn = cnt[j];
             const double r = smax(0.0, res[j]);
-            if (cn > 0 && dmul(r, frecip(cn)) <= athr) inc = smin(inc, ddiv(r, (double)cn));
+            if (cn > 0 && dmul(r, frecip(cn)) <= athr) q = smin(q, ddiv(r, (double)cn));
           }
-          for (int m = G::N / 2; m > 0; m >>= 1) inc = smin(inc, g.shfl_xor(inc, m));
+          // quotients are >= +0 and cmin is never -0: min{cmin, q...} is order-free
+          inc = smin(inc, g.min_nonneg(q));
         }
         inc = smax(inc, 0.0);
         R = dadd(R, inc);
@@ -1842,7 +1834,7 @@ struct Engine {
             }
             nc2 += popc32(mk);
           }
-          for (int m = G::N / 2; m > 0; m >>= 1) mn = smin(mn, g.shfl_xor(mn, m));
+          mn = g.min_nonneg(mn);  // stored caps are smax(0, cap) >= 0
           g.sync();
           ncap = nc2;
           cmn = mn;

@@ -21,6 +21,18 @@
 #define MF_NOINLINE
 #endif
 
+// unroll factor of the lane-strided hot loops (A/B builds: -DMF_UNROLL_N=1)
+#ifndef MF_UNROLL_N
+#define MF_UNROLL_N 4
+#endif
+#define MF_PRAGMA_(x) _Pragma(#x)
+#define MF_PRAGMA(x) MF_PRAGMA_(x)
+#if defined(__CUDACC__)
+#define MF_UNROLL MF_PRAGMA(unroll MF_UNROLL_N)
+#else
+#define MF_UNROLL
+#endif
+
 namespace mfb {
 
 #if defined(__CUDACC__)
@@ -61,6 +73,38 @@ struct WarpLanes {
     const unsigned sh = (unsigned)(reinterpret_cast<uintptr_t>(p) & 3) * 8u;
     const unsigned old = atomicOr(w, 1u << sh);
     return (old >> sh) & 0xffu;
+  }
+  // Warp minimum of a NON-NEGATIVE, non-NaN double (+0 <= x <= +inf). Such
+  // values order like their IEEE bit patterns read as unsigned integers, so two
+  // 32-bit redux.sync steps (high word, then low word among the lanes holding
+  // the minimal high word) replace a 5-step shuffle/compare butterfly. The
+  // result is the same IEEE value (bit pattern) on every lane.
+  MF_FN double min_nonneg(double v) const {
+    const unsigned long long b = (unsigned long long)__double_as_longlong(v);
+    const unsigned hi = (unsigned)(b >> 32), lo = (unsigned)b;
+    const unsigned mh = __reduce_min_sync(0xffffffffu, hi);
+    const unsigned ml = __reduce_min_sync(0xffffffffu, hi == mh ? lo : 0xffffffffu);
+    return __longlong_as_double((long long)(((unsigned long long)mh << 32) | ml));
+  }
+  MF_FN unsigned long long min_u64(unsigned long long v) const {
+    const unsigned hi = (unsigned)(v >> 32), lo = (unsigned)v;
+    const unsigned mh = __reduce_min_sync(0xffffffffu, hi);
+    const unsigned ml = __reduce_min_sync(0xffffffffu, hi == mh ? lo : 0xffffffffu);
+    return ((unsigned long long)mh << 32) | ml;
+  }
+  // Lexicographic warp argmin of (t, k) for t >= 0 or t == -0 (no NaN; -0 and
+  // +0 compare equal as with `<`/`==`): the lowest lane holding the minimal
+  // (t, k) wins; returns that lane's (t, k, payload) on every lane.
+  MF_FN void argmin_tk(double* t, unsigned long long* k, int* payload) const {
+    const double tc = *t + 0.0;  // -0 -> +0 (round-to-nearest)
+    const unsigned long long tb = (unsigned long long)__double_as_longlong(tc);
+    const unsigned long long tm = min_u64(tb);
+    const unsigned long long km = min_u64(tb == tm ? *k : ~0ull);
+    const unsigned win = __ballot_sync(0xffffffffu, tb == tm && *k == km);
+    const int src = __ffs(win) - 1;
+    *t = __shfl_sync(0xffffffffu, *t, src);
+    *k = km;
+    *payload = __shfl_sync(0xffffffffu, *payload, src);
   }
   // exclusive prefix sum of v over lanes; *total receives the warp sum
   MF_FN int excl_scan(int v, int* total) const {
@@ -113,6 +157,9 @@ struct SerialLanes {
     *total = v;
     return 0;
   }
+  inline double min_nonneg(double v) const { return v; }
+  inline unsigned long long min_u64(unsigned long long v) const { return v; }
+  inline void argmin_tk(double*, unsigned long long*, int*) const {}
 };
 
 }  // namespace mfb

@@ -38,7 +38,10 @@ class Fabric {
   const std::vector<Link>& links() const { return links_; }
 
   static Fabric star(int hosts, double capacity);
-  static Fabric fat_tree(int hosts, double capacity);
+  // oversub >= 1 divides the capacity of every switch-to-switch link (edge-agg
+  // and agg-core); 1 is the reference's uniform fabric (topology.cpp:108-145).
+  // Oversubscription is an oracle extension: the reference has no such key.
+  static Fabric fat_tree(int hosts, double capacity, double oversub = 1.0);
   static Fabric from(const Config& cfg);
 
  private:
