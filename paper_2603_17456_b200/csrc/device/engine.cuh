@@ -1721,62 +1721,131 @@ MF_UNROLL
       if (nt > s.max_touch) s.max_touch = nt;
       int nu = n;
       double R = 0.0;
+      // Register tile: when the touched slots fit G::N * kTile, lane l owns
+      // tile positions l, l + N, ... (slot id, residual, count) for the whole
+      // class, so a round reads only the counts the freeze pass may have
+      // changed. Same operations in the same per-slot order as the shared-
+      // memory loop below; residuals go back to shared memory at class end.
+      constexpr int kTile = G::N == 1 ? 32 : 128 / G::N;  // 32-bit live mask
+      const bool tiled = nt <= G::N * kTile;
+      const int n_tile0 = nt;
+      int tj[kTile], tc[kTile];
+      double tr[kTile];
+      unsigned live = 0u;  // bit m: tile entry m is still a touched slot
+      if (tiled) {
+#pragma unroll
+        for (int m = 0; m < kTile; ++m) {
+          const int jj = g.lane() + m * G::N;
+          tj[m] = 0;
+          tr[m] = 0.0;
+          tc[m] = 0;
+          if (jj < nt) {
+            tj[m] = tl[jj];
+            tr[m] = res[tj[m]];
+            live |= 1u << m;
+          }
+        }
+      }
       while (nu > 0) {
         ++rounds;
         MF_TIC(q2);
         const double cmin = ncap > 0 ? dsub(cmn, R) : MF_INF;
-        double amin = MF_INF;
-MF_UNROLL
-        for (int jj = g.lane(); jj < nt; jj += G::N) {
-          const int j = tl[jj];
-          const int cn = cnt[j];
-          const double r = res[j];
-          if (cn > 0) amin = smin(amin, dmul(smax(0.0, r), frecip(cn)));
-        }
-        amin = g.min_nonneg(amin);  // smax(0, r) / cnt >= 0
         double inc = cmin;
-        if (amin <= cmin) {  // exact quotients only within the approximation margin
-          const double athr = dadd(amin, dmul(amin, 0x1p-18));
-          double q = MF_INF;
+        int ns = 0, nt2 = 0;
+        if (tiled) {
+          double amin = MF_INF;
+#pragma unroll
+          for (int m = 0; m < kTile; ++m) {
+            if (live & (1u << m)) {
+              tc[m] = cnt[tj[m]];  // the previous round's freezes lowered some
+              if (tc[m] > 0) amin = smin(amin, dmul(smax(0.0, tr[m]), frecip(tc[m])));
+            }
+          }
+          amin = g.min_nonneg(amin);
+          if (amin <= cmin) {
+            const double athr = dadd(amin, dmul(amin, 0x1p-18));
+            double q = MF_INF;
+#pragma unroll
+            for (int m = 0; m < kTile; ++m) {
+              if ((live & (1u << m)) && tc[m] > 0) {
+                const double r = smax(0.0, tr[m]);
+                if (dmul(r, frecip(tc[m])) <= athr) q = smin(q, ddiv(r, (double)tc[m]));
+              }
+            }
+            inc = smin(inc, g.min_nonneg(q));
+          }
+          inc = smax(inc, 0.0);
+          R = dadd(R, inc);
+          MF_TOC(OUT_CY_SUB + 2, q2);
+          MF_TIC(q3);
+#pragma unroll
+          for (int m = 0; m < kTile; ++m) {
+            bool st = false, lv = false;
+            if ((live & (1u << m)) && tc[m] > 0) {
+              const double r = dsub(tr[m], dmul(inc, (double)tc[m]));
+              tr[m] = r;
+              st = r <= s.sat_max && r <= dmul(1e-12, capv[slink[tj[m]]]);
+              lv = !st;
+            }
+            // tile order m-major then lane == the shared loop's tl order
+            const unsigned ms = g.ballot(st);
+            if (st) sat[ns + popc32(ms & g.lanemask_lt())] = (unsigned short)tj[m];
+            ns += popc32(ms);
+            nt2 += popc32(g.ballot(lv));
+            live = lv ? (live | (1u << m)) : (live & ~(1u << m));
+          }
+        } else {
+          double amin = MF_INF;
 MF_UNROLL
           for (int jj = g.lane(); jj < nt; jj += G::N) {
             const int j = tl[jj];
             const int cn = cnt[j];
-            const double r = smax(0.0, res[j]);
-            if (cn > 0 && dmul(r, frecip(cn)) <= athr) q = smin(q, ddiv(r, (double)cn));
+            const double r = res[j];
+            if (cn > 0) amin = smin(amin, dmul(smax(0.0, r), frecip(cn)));
           }
-          // quotients are >= +0 and cmin is never -0: min{cmin, q...} is order-free
-          inc = smin(inc, g.min_nonneg(q));
-        }
-        inc = smax(inc, 0.0);
-        R = dadd(R, inc);
-        MF_TOC(OUT_CY_SUB + 2, q2);
-        MF_TIC(q3);
-        // residual update; saturated slots collected, drained slots dropped
-        int ns = 0, nt2 = 0;
-        for (int base = 0; base < nt; base += G::N) {
-          const int jj = base + g.lane();
-          int j = 0;
-          bool st = false, live = false;
-          if (jj < nt) {
-            j = tl[jj];
-            const int cn = cnt[j];
-            if (cn > 0) {
-              const double r = dsub(res[j], dmul(inc, (double)cn));
-              res[j] = r;
-              // r <= 1e-12 * cap_j implies r <= sat_max (rounding is monotone):
-              // the capacity is loaded only for the rare candidates
-              st = r <= s.sat_max && r <= dmul(1e-12, capv[slink[j]]);
-              live = !st;
+          amin = g.min_nonneg(amin);  // smax(0, r) / cnt >= 0
+          if (amin <= cmin) {  // exact quotients only within the approximation margin
+            const double athr = dadd(amin, dmul(amin, 0x1p-18));
+            double q = MF_INF;
+MF_UNROLL
+            for (int jj = g.lane(); jj < nt; jj += G::N) {
+              const int j = tl[jj];
+              const int cn = cnt[j];
+              const double r = smax(0.0, res[j]);
+              if (cn > 0 && dmul(r, frecip(cn)) <= athr) q = smin(q, ddiv(r, (double)cn));
             }
+            // quotients are >= +0 and cmin is never -0: min{cmin, q...} is order-free
+            inc = smin(inc, g.min_nonneg(q));
           }
-          g.sync();  // all lanes read tl[jj] before the in-place compaction
-          const unsigned ms = g.ballot(st);
-          if (st) sat[ns + popc32(ms & g.lanemask_lt())] = (unsigned short)j;
-          ns += popc32(ms);
-          const unsigned ml = g.ballot(live);
-          if (live) tl[nt2 + popc32(ml & g.lanemask_lt())] = (unsigned short)j;
-          nt2 += popc32(ml);
+          inc = smax(inc, 0.0);
+          R = dadd(R, inc);
+          MF_TOC(OUT_CY_SUB + 2, q2);
+          MF_TIC(q3);
+          // residual update; saturated slots collected, drained slots dropped
+          for (int base = 0; base < nt; base += G::N) {
+            const int jj = base + g.lane();
+            int j = 0;
+            bool st = false, lv = false;
+            if (jj < nt) {
+              j = tl[jj];
+              const int cn = cnt[j];
+              if (cn > 0) {
+                const double r = dsub(res[j], dmul(inc, (double)cn));
+                res[j] = r;
+                // r <= 1e-12 * cap_j implies r <= sat_max (rounding is monotone):
+                // the capacity is loaded only for the rare candidates
+                st = r <= s.sat_max && r <= dmul(1e-12, capv[slink[j]]);
+                lv = !st;
+              }
+            }
+            g.sync();  // all lanes read tl[jj] before the in-place compaction
+            const unsigned ms = g.ballot(st);
+            if (st) sat[ns + popc32(ms & g.lanemask_lt())] = (unsigned short)j;
+            ns += popc32(ms);
+            const unsigned ml = g.ballot(lv);
+            if (lv) tl[nt2 + popc32(ml & g.lanemask_lt())] = (unsigned short)j;
+            nt2 += popc32(ml);
+          }
         }
         g.sync();
         MF_TOC(OUT_CY_SUB + 3, q3);
@@ -1855,7 +1924,15 @@ MF_UNROLL
         nt = nt2;
       }
       // slot counts of this class are back to zero (every member froze)
-      for (int jj = g.lane(); jj < nt; jj += G::N) cnt[tl[jj]] = 0;
+      if (tiled) {
+#pragma unroll
+        for (int m = 0; m < kTile; ++m) {
+          if (g.lane() + m * G::N < n_tile0) res[tj[m]] = tr[m];
+          if (live & (1u << m)) cnt[tj[m]] = 0;
+        }
+      } else {
+        for (int jj = g.lane(); jj < nt; jj += G::N) cnt[tl[jj]] = 0;
+      }
       g.sync();
     }
     s.classes += ncls;
