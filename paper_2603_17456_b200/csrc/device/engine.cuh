@@ -172,9 +172,11 @@ struct Sc {
 
 #if defined(MF_PROF) && defined(__CUDACC__)
 #define MF_TIC(v) long long v = clock64()
+#define MF_RETIC(v) v = clock64()
 #define MF_TOC(slot, v) s.cy[slot - OUT_CY_NEXT] += clock64() - v
 #else
 #define MF_TIC(v)
+#define MF_RETIC(v)
 #define MF_TOC(slot, v)
 #endif
 
@@ -1752,6 +1754,7 @@ MF_UNROLL
         const double cmin = ncap > 0 ? dsub(cmn, R) : MF_INF;
         double inc = cmin;
         int ns = 0, nt2 = 0;
+        MF_TIC(q3);
         if (tiled) {
           double amin = MF_INF;
 #pragma unroll
@@ -1777,7 +1780,7 @@ MF_UNROLL
           inc = smax(inc, 0.0);
           R = dadd(R, inc);
           MF_TOC(OUT_CY_SUB + 2, q2);
-          MF_TIC(q3);
+          MF_RETIC(q3);
 #pragma unroll
           for (int m = 0; m < kTile; ++m) {
             bool st = false, lv = false;
@@ -1820,7 +1823,7 @@ MF_UNROLL
           inc = smax(inc, 0.0);
           R = dadd(R, inc);
           MF_TOC(OUT_CY_SUB + 2, q2);
-          MF_TIC(q3);
+          MF_RETIC(q3);
           // residual update; saturated slots collected, drained slots dropped
           for (int base = 0; base < nt; base += G::N) {
             const int jj = base + g.lane();

@@ -21,9 +21,10 @@
 #define MF_NOINLINE
 #endif
 
-// unroll factor of the lane-strided hot loops (A/B builds: -DMF_UNROLL_N=1)
+// unroll factor of the lane-strided hot loops: 1 measured fastest (icache-bound;
+// A/B of 1/2/4 on the bench workload, profiles/r01_ab_engine_builds.txt)
 #ifndef MF_UNROLL_N
-#define MF_UNROLL_N 4
+#define MF_UNROLL_N 1
 #endif
 #define MF_PRAGMA_(x) _Pragma(#x)
 #define MF_PRAGMA(x) MF_PRAGMA_(x)
