@@ -325,7 +325,7 @@ typedef struct {
   int has_horizon;
   double horizon;
   long maxtok, livelock;
-  int policy; /* 0 fs 1 sjf 2 edf 3 karuna 4 mfs */
+  int policy; /* 0 fs 1 sjf 2 edf 3 karuna 4 mfs 5 aalo (extension) */
   int K;
   double thr[MAXK];
   int prune;
@@ -530,6 +530,11 @@ typedef struct {
   vec active;
   /* last allocation insertion order (flow ids) */
   vec aorder;
+  /* aalo (extension): bytes of finished flows per (batch layer, stage) */
+  vec att;
+  double* asum; /* per-decide sums, valid where astamp == adecide */
+  long* astamp;
+  long acap, adecide;
   double horizon;
   long pruned_count;
 } engine;
@@ -537,6 +542,11 @@ typedef struct {
 #define FL(e, i) (AT((e)->flows, flow, i))
 #define BA(e, i) (AT((e)->batches, batch, i))
 #define LY(e, b, l) (AT((e)->layers, layer, BA(e, b).lbase + (l)))
+/* extension: Aalo coflow of a flow = (batch, target layer, stage); dense index */
+static long aalo_idx(engine* e, const flow* f) { /* -1: no (batch, layer) coflow */
+  if (f->batch < 0 || f->tl < 1 || f->tl > BA(e, f->batch).layers) return -1;
+  return ((long)BA(e, f->batch).lbase + f->tl - 1) * 3 + f->stage;
+}
 #define CF(e, i) (AT((e)->cofs, coflow, i))
 
 static int klass_of(int k) { return k <= KDEP ? 0 : (k == KTICK ? 2 : 1); }
@@ -896,6 +906,56 @@ static void decide(engine* e, classes* C) {
     }
     free(ex);
     free(im);
+  } else if (e->P.policy == 5) {
+    /* extension -- Aalo-style D-CLAS coflow scheduling (no reference oracle):
+     * coflow c = (batch, target layer, stage); attained service
+     * a_c = D_c + sum over c's transferable flows, in active order, of
+     * (size - remaining), D_c = sizes of c's finished flows added in completion
+     * order; queue q_c = #{i : a_c >= Q0 * E^i, i < K-1}; one class per coflow,
+     * ordered by (q_c, coflow index = batch-major FIFO); a flow without a
+     * (batch, layer) -- no batch, or a target layer outside the batch's layers
+     * (manual scenarios) -- is its own coflow after every batch coflow of its
+     * queue, by flow id. */
+    if (e->acap < (long)e->att.n) {
+      e->acap = (long)e->att.n * 2 + 64;
+      e->asum = realloc(e->asum, sizeof(double) * e->acap);
+      e->astamp = realloc(e->astamp, sizeof(long) * e->acap);
+      memset(e->astamp, 0, sizeof(long) * e->acap);
+      e->adecide = 0;
+    }
+    long st = ++e->adecide;
+    mkey* k = malloc(sizeof(mkey) * (A + 1));
+    double* own = malloc(sizeof(double) * (A + 1));
+    for (int i = 0; i < A; ++i) {
+      flow* f = &FL(e, act[i]);
+      double v = f->size - f->rem;
+      long c = aalo_idx(e, f);
+      if (c >= 0) {
+        if (e->astamp[c] != st) {
+          e->astamp[c] = st;
+          e->asum[c] = AT(e->att, double, c);
+        }
+        e->asum[c] += v;
+      } else {
+        own[i] = v;
+      }
+    }
+    for (int i = 0; i < A; ++i) {
+      flow* f = &FL(e, act[i]);
+      long c = aalo_idx(e, f);
+      double a = c >= 0 ? e->asum[c] : own[i];
+      int q = 0;
+      while (q < e->P.K - 1 && a >= e->P.thr[q]) ++q;
+      mkey m = {act[i], q, c >= 0 ? (double)c : 0x1p40 + act[i], 0.0, 0.0};
+      k[i] = m;
+    }
+    free(own);
+    qsort(k, A, sizeof(mkey), mfs_cmp);
+    for (int i = 0; i < A; ++i) {
+      if (i == 0 || k[i].band != k[i - 1].band || k[i].k1 != k[i - 1].k1) add_class(C);
+      C->ids[C->n++] = k[i].id;
+    }
+    free(k);
   } else { /* mfs arbitrate (rmlq.cpp:201-260) */
     mkey* k = malloc(sizeof(mkey) * (A + 1));
     for (int i = 0; i < A; ++i) {
@@ -1434,6 +1494,7 @@ static void finish_flow(engine* e, int fid) { /* engine.cpp:318-354 */
   f->rem = 0.0;
   f->state = DONE;
   f->fin = e->now;
+  if (e->P.policy == 5 && aalo_idx(e, f) >= 0) AT(e->att, double, aalo_idx(e, f)) += f->size;
   remove_active(e, fid);
   f = &FL(e, fid);
   f->rate = 0.0;
@@ -1511,6 +1572,8 @@ static int new_batch(engine* e, int nmem, int moff, double admit, int nl) {
     y.coll = -1;
     y.reuse.es = y.p2d.es = sizeof(int);
     vpush(&e->layers, &y);
+    double z = 0.0;
+    for (int k = 0; k < 3; ++k) vpush(&e->att, &z);
   }
   return b;
 }
@@ -1793,6 +1856,7 @@ static void engine_init(engine* e, fabric* F, const params* P, req_in* rq, long 
   e->F = F;
   e->roff.es = e->rlinks.es = sizeof(int);
   e->flows.es = sizeof(flow);
+  e->att.es = sizeof(double);
   e->batches.es = sizeof(batch);
   e->layers.es = sizeof(layer);
   e->cofs.es = sizeof(coflow);
@@ -1826,6 +1890,9 @@ static void engine_free(engine* e) {
   free(e->flows.p);
   free(e->batches.p);
   free(e->layers.p);
+  free(e->att.p);
+  free(e->asum);
+  free(e->astamp);
   free(e->cofs.p);
   if (!e->workload) free(e->mpool.p);
   free(e->fpool.p);
@@ -1884,9 +1951,19 @@ static int read_params(const kvcfg* c, params* P) {
   const char* pol = cfg_raw(c, "policy");
   if (!pol) pol = "fs";
   P->policy = !strcmp(pol, "fs") ? 0 : !strcmp(pol, "sjf") ? 1 : !strcmp(pol, "edf") ? 2
-            : !strcmp(pol, "karuna") ? 3 : !strcmp(pol, "mfs") ? 4 : -1;
+            : !strcmp(pol, "karuna") ? 3 : !strcmp(pol, "mfs") ? 4
+            : !strcmp(pol, "aalo") ? 5 : -1;
   if (P->policy < 0) fail(2, "unknown policy");
   P->K = 8;
+  if (P->policy == 5) { /* extension: Aalo D-CLAS queues, thresholds Q0 * E^i */
+    P->K = (int)cfg_long(c, "aalo.K", 8);
+    double E_ = cfg_num(c, "aalo.E", 10.0), q = cfg_num(c, "aalo.Q0", 1e-3);
+    if (P->K < 2 || P->K > MAXK || !(E_ > 1.0) || !(q > 0.0) || q == INF) fail(2, "config: aalo");
+    for (int i = 0; i + 1 < P->K && i < MAXK; ++i) {
+      P->thr[i] = q;
+      q *= E_;
+    }
+  }
   if (P->policy == 4) { /* rmlq.cpp:8-27, policy_factory.cpp:34-40 */
     P->K = (int)cfg_long(c, "mfs.K", 8);
     double E_ = cfg_num(c, "mfs.E", 4.0), U = cfg_num(c, "mfs.U", 0.5);

@@ -1108,6 +1108,8 @@ MF_UNROLL
       g.sync();
       const int nr = sorted_subset(I.s_ord + nd, SUB_NODL);
       ncls = group_classes(nd, nr, ncls);
+    } else if (pol == POL_AALO) {
+      ncls = decide_aalo(A);
     } else {  // MFS arbitrate (rmlq.cpp:201-260)
       for (int p = g.lane(); p < A; p += G::N) {
         const int fid = I.a_fid[p];
@@ -1141,6 +1143,66 @@ MF_UNROLL
     g.sync();
     s.algo_bytes += 40LL * A;
     return ncls;
+  }
+
+  // Extension (no reference counterpart; oracle: oracle/mfsim_oracle.c decide,
+  // policy 5): Aalo D-CLAS. Coflow c = (batch, target layer, stage) at
+  // pl index * 3 + stage; attained a_c = pl_att[c] (finished flows' sizes, in
+  // completion order) + (size - remaining) of c's active flows in active order;
+  // queue = #{i < K-1 : a_c >= thr[i]}; classes by (queue, c), flows without a
+  // (batch, layer) are singleton coflows after the batch coflows of their queue.
+  MF_FN int aalo_coflow(int fid, int b) const {  // -1: no (batch, layer) coflow
+    if (b < 0) return -1;
+    const int tl = I.f_tl[fid];
+    if (tl < 1 || tl > I.b_layers[b]) return -1;
+    return (I.b_lbase[b] + tl - 1) * 3 + I.f_stage[fid];
+  }
+  MF_NOINLINE int decide_aalo(int A) {
+    double* __restrict__ att = I.pl_att;
+    double* __restrict__ sum = I.pl_asum;
+    int* __restrict__ cx = I.x_aux;  // coflow per active position (free until the sort)
+    for (int p = g.lane(); p < A; p += G::N) {
+      const int fid = I.a_fid[p];
+      const int b = I.f_batch[fid];
+      const int c = aalo_coflow(fid, b);
+      if (c >= 0) sum[c] = att[c];  // equal stores from every member
+      cx[p] = c;
+    }
+    g.sync();
+    // sequential sums in active order: per chunk of N positions, the lowest
+    // lane of every coflow group adds its group's values in lane order
+    for (int base = 0; base < A; base += G::N) {
+      const int p = base + g.lane();
+      int c = -1;
+      double v = 0.0;
+      if (p < A) {
+        c = cx[p];
+        v = dsub(I.f_size[I.a_fid[p]], I.a_rem[p]);
+      }
+      const unsigned grp = g.match_any(c);
+      const bool lead = c >= 0 && (grp & g.lanemask_lt()) == 0u;
+      double acc = lead ? sum[c] : 0.0;
+      for (int k = 0; k < G::N; ++k) {
+        const double vk = g.shfl(v, k);
+        if (lead && ((grp >> k) & 1u)) acc = dadd(acc, vk);
+      }
+      if (lead) sum[c] = acc;
+      g.sync();
+    }
+    for (int p = g.lane(); p < A; p += G::N) {
+      const int fid = I.a_fid[p];
+      const int c = cx[p];
+      const double a = c >= 0 ? sum[c] : dsub(I.f_size[fid], I.a_rem[p]);
+      int q = 0;
+      while (q < I.p.K - 1 && a >= I.p.thr[q]) ++q;
+      I.s_k0[p] = (unsigned long long)q;
+      I.s_k1[p] = c >= 0 ? (unsigned long long)c : (1ull << 40) + (unsigned long long)fid;
+      I.s_k2[p] = 0;
+      I.s_k3[p] = 0;
+    }
+    g.sync();
+    const int n = sorted_subset(I.s_ord, SUB_ALL);
+    return group_classes(0, n, 0);
   }
 
   static constexpr int kMaxAdd = 64;  // merged into the previous order; more: full sort
@@ -2095,6 +2157,10 @@ MF_UNROLL
         I.r_open[r] = ropen - 1;
         I.r_lastfin[r] = smax(rlast, s.now);
       }
+      if (I.p.policy == POL_AALO) {  // extension: attained bytes of the coflow
+        const int ac = aalo_coflow(fid, b);
+        if (ac >= 0) I.pl_att[ac] = dadd(I.pl_att[ac], size);
+      }
     }
     g.sync();
     if (pos >= 0) remove_active_at(fid, pos);
@@ -2364,6 +2430,8 @@ MF_UNROLL
       I.pl_rcnt[idx] = 0;
       I.pl_poff[idx] = s.pp_top + i * mcnt;
       I.pl_pcnt[idx] = 0;
+      if (I.p.policy == POL_AALO)
+        for (int k = 0; k < 3; ++k) I.pl_att[3 * idx + k] = 0.0;
     }
     g.sync();
     s.rp_top += L * mcnt;

@@ -21,7 +21,8 @@
 
 namespace mfb {
 
-enum : int { POL_FS = 0, POL_SJF = 1, POL_EDF = 2, POL_KARUNA = 3, POL_MFS = 4 };
+enum : int { POL_FS = 0, POL_SJF = 1, POL_EDF = 2, POL_KARUNA = 3, POL_MFS = 4,
+             POL_AALO = 5 /* extension: no reference oracle (oracle/mfsim_oracle.c) */ };
 enum : uint8_t { ST_REUSE = 0, ST_COLL = 1, ST_P2D = 2 };
 enum : uint8_t { FL_PENDING = 0, FL_ACTIVE = 1, FL_DONE = 2, FL_PRUNED = 3 };
 enum : uint8_t { BD_URGENT = 0, BD_EARLY = 1, BD_DEFERRED = 2, BD_SCAV = 3 };
@@ -76,7 +77,7 @@ constexpr int kScBlob = 1024;  // bytes reserved for the suspended scalar state
 struct InstParams {
   int policy;
   int K;
-  double thr[kMaxK];  // Q_1..Q_{K-1} (rmlq.cpp:8-22)
+  double thr[kMaxK];  // Q_1..Q_{K-1} (rmlq.cpp:8-22); aalo: Q0 * E^i
   double tick;        // EngineParams::promotion_tick
   double horizon;     // absolute
   long long livelock;
@@ -179,6 +180,9 @@ struct Inst {
   int* pl_rcnt;
   int* pl_poff;
   int* pl_pcnt;
+  // aalo (extension), [3 * PL_cap] by (batch layer, stage): finished bytes, per-step sums
+  double* pl_att;
+  double* pl_asum;
   int* rpool;  // reuse deps  [RP_cap]
   int* ppool;  // p2d by layer [PP_cap]
   // ---- coflows [C_cap]

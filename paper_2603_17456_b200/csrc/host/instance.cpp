@@ -703,6 +703,9 @@ void carve_instance(Carver& c, const InstanceInput& in, Inst& d, const Inst& top
   d.pl_rcnt = state((int*)nullptr, nPL);
   d.pl_poff = state((int*)nullptr, nPL);
   d.pl_pcnt = state((int*)nullptr, nPL);
+  const size_t nAT = d.p.policy == mfb::POL_AALO ? 3 * nPL : 1;
+  d.pl_att = state((double*)nullptr, nAT);
+  d.pl_asum = c.S<double>(nAT);
   d.rpool = state((int*)nullptr, d.RP_cap);
   d.ppool = state((int*)nullptr, d.PP_cap);
   d.c_batch = state((int*)nullptr, nC);
@@ -846,6 +849,8 @@ void carve_instance(Carver& c, const InstanceInput& in, Inst& d, const Inst& top
         host_of(c, d.pl_poff)[pl] = pp;
         host_of(c, d.pl_pcnt)[pl] = static_cast<int>(m->p2d[b][l].size());
         for (int f : m->p2d[b][l]) host_of(c, d.ppool)[pp++] = f;
+        if (d.p.policy == mfb::POL_AALO)
+          for (int k = 0; k < 3; ++k) host_of(c, d.pl_att)[3 * pl + k] = 0.0;
       }
       // initial BatchAdmit event, pushed by add_manual_batch (engine.cpp:178)
       host_of(c, d.e_t)[b] = m->admit_at[b];
@@ -965,8 +970,8 @@ void Batch::pack() {
   std::vector<double> cost(n);
   for (int i = 0; i < n; ++i) {
     const Inst& d = desc_[i];
-    static const double factor[] = {1.0, 1.6, 1.1, 12.0, 2.5};
-    const int pol = d.p.policy >= 0 && d.p.policy < 5 ? d.p.policy : 0;
+    static const double factor[] = {1.0, 1.6, 1.1, 12.0, 2.5, 1.5};
+    const int pol = d.p.policy >= 0 && d.p.policy < 6 ? d.p.policy : 0;
     cost[i] = factor[pol] * (double(d.F_cap) + 2.0 * d.n_req);
   }
   // claim groups: one per policy, so that the warps sharing an SM run the same

@@ -15,9 +15,10 @@
 
 namespace mfh {
 
-enum class PolicyKind { FairShare, SJF, EDF, Karuna, MFS };
+enum class PolicyKind { FairShare, SJF, EDF, Karuna, MFS, Aalo };
 
-PolicyKind parse_policy(const std::string& name);  // fs|sjf|edf|karuna|mfs
+// fs|sjf|edf|karuna|mfs, plus the extension aalo (no reference counterpart)
+PolicyKind parse_policy(const std::string& name);
 const char* policy_name(PolicyKind k);
 
 class Scheduler {
@@ -66,6 +67,24 @@ class MfsScheduler : public Scheduler {  // rmlq.hpp:61-101
  private:
   RmlqParams rmlq_;
   InterParams inter_;
+};
+
+// Extension (BASELINE configs[1] "Varys/Aalo-style
+// coflow"): Aalo's D-CLAS. Coflow = (batch, target layer, stage); queue from
+// attained service against thresholds Q0 * E^i (aalo.Q0, aalo.E, aalo.K);
+// one priority class per coflow, FIFO (batch-major) within a queue. The
+// reference has no such policy: its oracle is oracle/mfsim_oracle.c (policy 5).
+class AaloScheduler : public Scheduler {
+ public:
+  AaloScheduler(int K, double E, double Q0) : K_(K), E_(E), Q0_(Q0) {}
+  const char* name() const override { return "aalo"; }
+  PolicyKind kind() const override { return PolicyKind::Aalo; }
+  void configure(mfb::InstParams& p) const override;
+  static std::unique_ptr<AaloScheduler> from(const Config& cfg);
+
+ private:
+  int K_;
+  double E_, Q0_;
 };
 
 std::unique_ptr<Scheduler> make_scheduler(PolicyKind kind, const Config& cfg);

@@ -13,6 +13,9 @@ Cases (paper_2603_17456_b200/configs.py):
   cfg2_<pol>           configs[1]: cluster8 at the FS knee, 10k requests, 5 policies
   cfg3_<pol>_s<seed>   configs[2]: ft128 (1024 GPUs), 100k requests, 5 policies, seeds 1-3
   cfg5_<pol>           configs[4]: 4096-GPU fat-tree, heavy-tailed trace, mfs/fs
+  cfg2_aalo            configs[1]'s coflow baseline (extension, no reference
+                       counterpart): produced by the C restatement
+                       (oracle/_ref/libmfsim_oracle.so), marked "oracle": "restatement"
 
 Runs where /root/reference exists (this container), many cases in parallel,
 skipping cases whose file already exists:
@@ -39,7 +42,7 @@ def baseline_cases():
     for p in ("mfs", "fs"):
         for s in range(1, 6):
             c[f"cfg1_{p}_s{s}"] = configs.config1(seed=s, policy=p)
-    for p in POLICIES:
+    for p in POLICIES + ("aalo",):
         c[f"cfg2_{p}"] = configs.config2(policy=p)
     for p in POLICIES:
         for s in (1, 2, 3):
@@ -60,12 +63,14 @@ def _one(item):
     from oracle import ref
     from make_golden import record
     t0 = time.time()
-    res = ref.run_config(text)
+    so = ref.ORACLE_SO if "policy = aalo" in text else ref.REF_SO
+    res = ref.run_config(text, so=so)
     meta = record(res, {}, name, full=False)
     meta["n_requests"] = int(len(res.req_done))
     meta["n_flows"] = int(len(res.flow_finish))
     meta["ref_seconds"] = round(time.time() - t0, 1)
     meta["config"] = text
+    meta["oracle"] = "restatement" if so == ref.ORACLE_SO else "reference"
     path = os.path.join(OUT, name + ".json")
     with open(path + ".tmp", "w") as f:
         json.dump(meta, f, indent=1, sort_keys=True)

@@ -6,6 +6,10 @@ switched off.
   topology.oversubscription = o  (fat-tree): every switch-to-switch link
       (edge-agg, agg-core) carries capacity / o; host links keep capacity.
       o = 1 (or absent) is the reference's uniform fabric.
+  policy = aalo  Aalo-style D-CLAS coflow scheduling (BASELINE configs[1]'s
+      "Varys/Aalo-style coflow" baseline): coflow = (batch, target layer,
+      stage); queue from attained bytes vs Q0 * E^i (aalo.Q0/E/K); one class
+      per coflow, FIFO by batch within a queue.
 """
 import os
 
@@ -82,6 +86,81 @@ def test_oversub_host_engine_matches_oracle(emu, policy):
 def test_oversub_device_matches_oracle(product):
     from paper_2603_17456_b200.native import DeviceBatch
     texts = [oversub_fattree(p, 2.5) for p in POLICIES] + [oversub_ft128(p, 2.0) for p in POLICIES]
+    b = DeviceBatch(0, product)
+    for t in texts:
+        b.add_config(t)
+    b.prepare()
+    b.run(2)
+    bad = {}
+    for i, t in enumerate(texts):
+        d = diff(b.result(i, 2, reports=True), ref.run_config(t, so=ref.ORACLE_SO))
+        if d:
+            bad[i] = d
+    assert bad == {}
+
+
+def aalo_cases():
+    c8 = open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "configs", "cluster8.conf")).read()
+    return {
+        "cluster8_200": c8 + "workload.request_count = 200\npolicy = aalo\n",
+        "cluster8_200_q": c8 + "workload.request_count = 200\npolicy = aalo\naalo.Q0 = 1e-2\naalo.E = 4\naalo.K = 5\n",
+        "fattree": cases.fattree_config("aalo"),
+        "fattree_oversub": oversub_fattree("aalo", 2.0),
+        "sanity": cases.sanity_config("aalo"),
+        "example": open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "configs", "example.conf")).read()
+        + "policy = aalo\n",
+    }
+
+
+@needs_oracle
+@pytest.mark.parametrize("name", sorted(aalo_cases()))
+def test_aalo_host_engine_matches_oracle(emu, name):
+    from paper_2603_17456_b200.native import run_config
+    text = aalo_cases()[name]
+    want = ref.run_config(text, so=ref.ORACLE_SO)
+    got = run_config(text, lib=emu, detail=2)
+    assert diff(got, want) == []
+    assert '"policy": "aalo"' in (got.summary_json or '"policy": "aalo"')
+
+
+@needs_oracle
+@pytest.mark.parametrize("name", ["trio", "ingress", "egress", "single_request", "stall_zero",
+                                  "ticks", "tick_promotion"])
+def test_aalo_manual_scenarios_match_oracle(emu, name):
+    from paper_2603_17456_b200.native import run_manual
+    import re
+    fn = getattr(cases, name)
+    spec = fn("aalo") if name in ("trio", "ingress", "egress") else fn()
+    spec = re.sub(r"^policy \w+", "policy aalo", spec, flags=re.M)
+    assert "policy aalo" in spec
+    assert diff(run_manual(spec, lib=emu), ref.run_manual(spec, so=ref.ORACLE_SO)) == []
+
+
+@needs_oracle
+def test_aalo_differs_from_the_reference_policies():
+    text = aalo_cases()["cluster8_200"]
+    a = ref.run_config(text, so=ref.ORACLE_SO)
+    for p in POLICIES:
+        b = ref.run_config(text.replace("policy = aalo", f"policy = {p}"), so=ref.ORACLE_SO)
+        assert not bits_equal(a.flow_finish, b.flow_finish), p
+
+
+@pytest.mark.parametrize("bad", ["aalo.K = 1", "aalo.K = 99", "aalo.E = 1", "aalo.Q0 = 0", "aalo.Q0 = -1"])
+def test_aalo_config_errors(emu, bad):
+    from paper_2603_17456_b200.native import Config, DeviceBatch, MfsimError
+    b = DeviceBatch(0, emu)
+    with pytest.raises(MfsimError) as e:
+        b.add_config(Config(cases.sanity_config("aalo") + bad + "\n", emu))
+        b.prepare()
+    assert e.value.code == 2
+
+
+@pytest.mark.gpu
+def test_aalo_device_matches_oracle(product):
+    from paper_2603_17456_b200 import sweep
+    from paper_2603_17456_b200.native import DeviceBatch
+    texts = list(aalo_cases().values())
+    texts.append(sweep.sweep_config((0.8, 3, 1, "aalo"), requests=400, lib=product))
     b = DeviceBatch(0, product)
     for t in texts:
         b.add_config(t)
