@@ -1372,48 +1372,41 @@ MF_UNROLL
     const int A = s.n_active;
     for (int p = g.lane(); p < A; p += G::N) I.s_cap[p] = MF_INF;
     g.sync();
-    int n = 0;
-    for (int base = 0; base < nd; base += G::N) {
-      const int i = base + g.lane();
-      int c = 0, p = -1;
+    // want = remaining / slack for positive slack; demand on the touched links zeroed
+    for (int i = g.lane(); i < nd; i += G::N) {
+      const int p = I.s_ord[i];
+      const double slack = dsub(I.f_dl[I.a_fid[p]], s.now);
+      if (slack > 0.0) {
+        I.s_cap[p] = ddiv(I.a_rem[p], slack);  // stash: capped below
+        const int rn = arn(p);
+        for (int k = 0; k < rn; ++k) I.l_x[arl(p, k)] = 0.0;
+      }
+    }
+    g.sync();
+    // per-link demand summed in deadline_ids (= active) order (baselines.cpp:112-118):
+    // flows one after another, each adding to its (distinct) route links in parallel
+    for (int i0 = 0; i0 < nd; i0 += G::N) {
+      const int i = i0 + g.lane();
+      int p = 0, rn = 0;
       double want = 0.0;
       if (i < nd) {
         p = I.s_ord[i];
-        const double slack = dsub(I.f_dl[I.a_fid[p]], s.now);
-        if (slack > 0.0) {
-          want = ddiv(I.a_rem[p], slack);
-          c = arn(p);
-        }
+        want = I.s_cap[p];
+        if (want < MF_INF) rn = arn(p);
       }
-      int tot;
-      const int off = g.excl_scan(c, &tot);
-      if (c > 0) {
-        for (int k = 0; k < c; ++k) {
-          I.x_seg[n + off + k] = entry_key(p, k);
-          I.x_hi[n + off + k] = 0;
-          I.x_val[n + off + k] = want;
-          I.x_aux[n + off + k] = 0;
+      const int cnt = nd - i0 < G::N ? nd - i0 : G::N;
+      for (int t = 0; t < cnt; ++t) {
+        const int rt = g.shfl(rn, t);
+        if (rt == 0) continue;
+        const int pt = g.shfl(p, t);
+        const double w = g.shfl(want, t);
+        for (int k = g.lane(); k < rt; k += G::N) {
+          const int l = arl(pt, k);
+          I.l_x[l] = dadd(I.l_x[l], w);
         }
-        I.s_cap[p] = want;  // stash: capped below
+        g.sync();
       }
-      n += tot;
     }
-    g.sync();
-    if (n > I.X_cap) {
-      fail(ERR_INTERNAL, CHK_CAP_SCRATCH);
-      return;
-    }
-    const int nt = bucket_by_link(n);
-    for (int j = g.lane(); j < nt; j += G::N) {
-      int e0, e1;
-      const int l = bucket_at(j, &e0, &e1);
-      double dmd = 0.0;
-MF_UNROLL
-      for (int a = e0; a < e1; ++a) dmd = dadd(dmd, I.y_val[a]);
-      I.l_x[l] = dmd;
-    }
-    g.sync();
-    bucket_release(nt);
     for (int i = g.lane(); i < nd; i += G::N) {
       const int p = I.s_ord[i];
       const double want = I.s_cap[p];
@@ -1636,6 +1629,98 @@ MF_UNROLL
   }
 
   // class filling with the shared class rate over the link slots
+  // Ascending sort of the capped entries (x_hi = cap bits, x_lo = active
+  // position) of one class, n <= kCapSort: a bitonic network over registers
+  // (8 entries per lane; lane-crossing stages by shuffle, register-crossing
+  // stages by static pairs). Caps are >= 0, so their bit patterns order like
+  // the values; equal caps may come out in any order (they freeze together).
+  static constexpr int kCapSort = 8 * G::N;
+  MF_FN static bool kv_gt(unsigned long long ha, unsigned la, unsigned long long hb, unsigned lb) {
+    return ha > hb || (ha == hb && la > lb);
+  }
+  MF_NOINLINE void sort_caps(int n) {
+    unsigned long long* __restrict__ xh = I.x_hi;
+    unsigned long long* __restrict__ xl = I.x_lo;
+    if (G::N == 1) {  // serial build: insertion sort
+      for (int i = 1; i < n; ++i) {
+        const unsigned long long h = xh[i], l = xl[i];
+        int j = i - 1;
+        while (j >= 0 && kv_gt((unsigned long long)xh[j], (unsigned)xl[j], h, (unsigned)l)) {
+          xh[j + 1] = xh[j];
+          xl[j + 1] = xl[j];
+          --j;
+        }
+        xh[j + 1] = h;
+        xl[j + 1] = l;
+      }
+      return;
+    }
+    constexpr int E = 8;
+    int n2 = G::N;
+    while (n2 < n) n2 <<= 1;
+    const int nm = n2 / G::N;
+    unsigned long long h[E];
+    unsigned lo[E];
+#pragma unroll
+    for (int m = 0; m < E; ++m) {
+      const int i = m * G::N + g.lane();
+      h[m] = i < n ? xh[i] : ~0ull;
+      lo[m] = i < n ? (unsigned)xl[i] : ~0u;
+    }
+#define MF_CS(a, b)                                                   \
+  if ((b) < nm) {                                                      \
+    const bool up = (((a)*G::N + g.lane()) & k) == 0;                  \
+    if (kv_gt(h[a], lo[a], h[b], lo[b]) == up) {                       \
+      const unsigned long long th = h[a];                              \
+      const unsigned tl_ = lo[a];                                      \
+      h[a] = h[b];                                                     \
+      lo[a] = lo[b];                                                   \
+      h[b] = th;                                                       \
+      lo[b] = tl_;                                                     \
+    }                                                                  \
+  }
+    for (int k = 2; k <= n2; k <<= 1) {
+      for (int j = k >> 1; j > 0; j >>= 1) {
+        if (j >= G::N) {
+          const int jm = j / G::N;
+          if (jm == 1) {
+            MF_CS(0, 1) MF_CS(2, 3) MF_CS(4, 5) MF_CS(6, 7)
+          } else if (jm == 2) {
+            MF_CS(0, 2) MF_CS(1, 3) MF_CS(4, 6) MF_CS(5, 7)
+          } else {
+            MF_CS(0, 4) MF_CS(1, 5) MF_CS(2, 6) MF_CS(3, 7)
+          }
+        } else {
+          const bool lower = (g.lane() & j) == 0;
+#pragma unroll
+          for (int m = 0; m < E; ++m) {
+            if (m < nm) {
+              const unsigned long long ph = g.shfl_xor(h[m], j);
+              const unsigned pl = (unsigned)g.shfl_xor((int)lo[m], j);
+              const bool up = ((m * G::N + g.lane()) & k) == 0;
+              const bool take = (lower == up) ? kv_gt(h[m], lo[m], ph, pl) : kv_gt(ph, pl, h[m], lo[m]);
+              if (take) {
+                h[m] = ph;
+                lo[m] = pl;
+              }
+            }
+          }
+        }
+      }
+    }
+#undef MF_CS
+    g.sync();
+#pragma unroll
+    for (int m = 0; m < E; ++m) {
+      const int i = m * G::N + g.lane();
+      if (m < nm && i < n) {
+        xh[i] = h[m];
+        xl[i] = lo[m];
+      }
+    }
+    g.sync();
+  }
+
   template <bool kLinksOnChip>
   MF_NOINLINE void allocate_slots(int ncls, bool has_caps) {
     const int A = s.n_active;
@@ -1783,134 +1868,69 @@ MF_UNROLL
       }
       MF_TOC(OUT_CY_SUB + 1, q1);
       if (nt > s.max_touch) s.max_touch = nt;
+      // capped members sorted by cap once per class (rounds then walk a prefix)
+      const bool csorted = ncap > 1 && ncap <= kCapSort;
+      const int ctot = ncap;
+      int cpos = 0;
+      if (csorted) sort_caps(ncap);
       int nu = n;
       double R = 0.0;
-      // Register tile: when the touched slots fit G::N * kTile, lane l owns
-      // tile positions l, l + N, ... (slot id, residual, count) for the whole
-      // class, so a round reads only the counts the freeze pass may have
-      // changed. Same operations in the same per-slot order as the shared-
-      // memory loop below; residuals go back to shared memory at class end.
-      constexpr int kTile = G::N == 1 ? 32 : 128 / G::N;  // 32-bit live mask
-      const bool tiled = nt <= G::N * kTile;
-      const int n_tile0 = nt;
-      int tj[kTile], tc[kTile];
-      double tr[kTile];
-      unsigned live = 0u;  // bit m: tile entry m is still a touched slot
-      if (tiled) {
-#pragma unroll
-        for (int m = 0; m < kTile; ++m) {
-          const int jj = g.lane() + m * G::N;
-          tj[m] = 0;
-          tr[m] = 0.0;
-          tc[m] = 0;
-          if (jj < nt) {
-            tj[m] = tl[jj];
-            tr[m] = res[tj[m]];
-            live |= 1u << m;
-          }
-        }
-      }
       while (nu > 0) {
         ++rounds;
         MF_TIC(q2);
         const double cmin = ncap > 0 ? dsub(cmn, R) : MF_INF;
+        double amin = MF_INF;
+MF_UNROLL
+        for (int jj = g.lane(); jj < nt; jj += G::N) {
+          const int j = tl[jj];
+          const int cn = cnt[j];
+          const double r = res[j];
+          if (cn > 0) amin = smin(amin, dmul(smax(0.0, r), frecip(cn)));
+        }
+        amin = g.min_nonneg(amin);  // smax(0, r) / cnt >= 0
         double inc = cmin;
-        int ns = 0, nt2 = 0;
-        MF_TIC(q3);
-        if (tiled) {
-          double amin = MF_INF;
-#pragma unroll
-          for (int m = 0; m < kTile; ++m) {
-            if (live & (1u << m)) {
-              tc[m] = cnt[tj[m]];  // the previous round's freezes lowered some
-              if (tc[m] > 0) amin = smin(amin, dmul(smax(0.0, tr[m]), frecip(tc[m])));
-            }
-          }
-          amin = g.min_nonneg(amin);
-          if (amin <= cmin) {
-            const double athr = dadd(amin, dmul(amin, 0x1p-18));
-            double q = MF_INF;
-#pragma unroll
-            for (int m = 0; m < kTile; ++m) {
-              if ((live & (1u << m)) && tc[m] > 0) {
-                const double r = smax(0.0, tr[m]);
-                if (dmul(r, frecip(tc[m])) <= athr) q = smin(q, ddiv(r, (double)tc[m]));
-              }
-            }
-            inc = smin(inc, g.min_nonneg(q));
-          }
-          inc = smax(inc, 0.0);
-          R = dadd(R, inc);
-          MF_TOC(OUT_CY_SUB + 2, q2);
-          MF_RETIC(q3);
-#pragma unroll
-          for (int m = 0; m < kTile; ++m) {
-            bool st = false, lv = false;
-            if ((live & (1u << m)) && tc[m] > 0) {
-              const double r = dsub(tr[m], dmul(inc, (double)tc[m]));
-              tr[m] = r;
-              st = r <= s.sat_max && r <= dmul(1e-12, capv[slink[tj[m]]]);
-              lv = !st;
-            }
-            // tile order m-major then lane == the shared loop's tl order
-            const unsigned ms = g.ballot(st);
-            if (st) sat[ns + popc32(ms & g.lanemask_lt())] = (unsigned short)tj[m];
-            ns += popc32(ms);
-            nt2 += popc32(g.ballot(lv));
-            live = lv ? (live | (1u << m)) : (live & ~(1u << m));
-          }
-        } else {
-          double amin = MF_INF;
+        if (amin <= cmin) {  // exact quotients only within the approximation margin
+          const double athr = dadd(amin, dmul(amin, 0x1p-18));
+          double q = MF_INF;
 MF_UNROLL
           for (int jj = g.lane(); jj < nt; jj += G::N) {
             const int j = tl[jj];
             const int cn = cnt[j];
-            const double r = res[j];
-            if (cn > 0) amin = smin(amin, dmul(smax(0.0, r), frecip(cn)));
+            const double r = smax(0.0, res[j]);
+            if (cn > 0 && dmul(r, frecip(cn)) <= athr) q = smin(q, ddiv(r, (double)cn));
           }
-          amin = g.min_nonneg(amin);  // smax(0, r) / cnt >= 0
-          if (amin <= cmin) {  // exact quotients only within the approximation margin
-            const double athr = dadd(amin, dmul(amin, 0x1p-18));
-            double q = MF_INF;
-MF_UNROLL
-            for (int jj = g.lane(); jj < nt; jj += G::N) {
-              const int j = tl[jj];
-              const int cn = cnt[j];
-              const double r = smax(0.0, res[j]);
-              if (cn > 0 && dmul(r, frecip(cn)) <= athr) q = smin(q, ddiv(r, (double)cn));
+          // quotients are >= +0 and cmin is never -0: min{cmin, q...} is order-free
+          inc = smin(inc, g.min_nonneg(q));
+        }
+        inc = smax(inc, 0.0);
+        R = dadd(R, inc);
+        MF_TOC(OUT_CY_SUB + 2, q2);
+        MF_TIC(q3);
+        // residual update; saturated slots collected, drained slots dropped
+        int ns = 0, nt2 = 0;
+        for (int base = 0; base < nt; base += G::N) {
+          const int jj = base + g.lane();
+          int j = 0;
+          bool st = false, live = false;
+          if (jj < nt) {
+            j = tl[jj];
+            const int cn = cnt[j];
+            if (cn > 0) {
+              const double r = dsub(res[j], dmul(inc, (double)cn));
+              res[j] = r;
+              // r <= 1e-12 * cap_j implies r <= sat_max (rounding is monotone):
+              // the capacity is loaded only for the rare candidates
+              st = r <= s.sat_max && r <= dmul(1e-12, capv[slink[j]]);
+              live = !st;
             }
-            // quotients are >= +0 and cmin is never -0: min{cmin, q...} is order-free
-            inc = smin(inc, g.min_nonneg(q));
           }
-          inc = smax(inc, 0.0);
-          R = dadd(R, inc);
-          MF_TOC(OUT_CY_SUB + 2, q2);
-          MF_RETIC(q3);
-          // residual update; saturated slots collected, drained slots dropped
-          for (int base = 0; base < nt; base += G::N) {
-            const int jj = base + g.lane();
-            int j = 0;
-            bool st = false, lv = false;
-            if (jj < nt) {
-              j = tl[jj];
-              const int cn = cnt[j];
-              if (cn > 0) {
-                const double r = dsub(res[j], dmul(inc, (double)cn));
-                res[j] = r;
-                // r <= 1e-12 * cap_j implies r <= sat_max (rounding is monotone):
-                // the capacity is loaded only for the rare candidates
-                st = r <= s.sat_max && r <= dmul(1e-12, capv[slink[j]]);
-                lv = !st;
-              }
-            }
-            g.sync();  // all lanes read tl[jj] before the in-place compaction
-            const unsigned ms = g.ballot(st);
-            if (st) sat[ns + popc32(ms & g.lanemask_lt())] = (unsigned short)j;
-            ns += popc32(ms);
-            const unsigned ml = g.ballot(lv);
-            if (lv) tl[nt2 + popc32(ml & g.lanemask_lt())] = (unsigned short)j;
-            nt2 += popc32(ml);
-          }
+          g.sync();  // all lanes read tl[jj] before the in-place compaction
+          const unsigned ms = g.ballot(st);
+          if (st) sat[ns + popc32(ms & g.lanemask_lt())] = (unsigned short)j;
+          ns += popc32(ms);
+          const unsigned ml = g.ballot(live);
+          if (live) tl[nt2 + popc32(ml & g.lanemask_lt())] = (unsigned short)j;
+          nt2 += popc32(ml);
         }
         g.sync();
         MF_TOC(OUT_CY_SUB + 3, q3);
@@ -1935,7 +1955,37 @@ MF_UNROLL
         // cap freezes (the same rate R, so the order against the link freezes
         // is immaterial): drop frozen entries, freeze cap - eps <= R, and take
         // the minimum cap of the survivors for the next round
-        if (ncap > 0) {
+        if (ncap > 0 && csorted) {
+          // cap-sorted entries: R >= cap - 1e-12 max(1, cap) holds on a prefix
+          // (the threshold is increasing in cap), so the pass is a pointer
+          // walk; entries frozen through a link are stepped over
+          for (;;) {
+            const int i = cpos + g.lane();
+            bool pass = false, fz = false;
+            int p = 0;
+            if (i < ctot) {
+              p = (int)I.x_lo[i];
+              const bool was = (frz[p >> 5] & (1u << (p & 31))) != 0u;
+              const double cp = bits_to_d(I.x_hi[i]);
+              fz = !was && R >= dsub(cp, dmul(1e-12, smax(1.0, cp)));
+              pass = was || fz;
+            }
+            const unsigned stop = g.ballot(!pass);
+            const int adv = stop ? ctz32(stop) : G::N;
+            if (fz && g.lane() < adv) {
+              g.atomic_or(&frz[p >> 5], 1u << (p & 31));
+              rate[p] = R;
+              const int rn = arnp[p];
+              for (int k = 0; k < rn; ++k) g.atomic_add(&cnt[asl[p * RM + k]], -1);
+              ++got;
+            }
+            cpos = cpos + adv < ctot ? cpos + adv : ctot;
+            if (stop || cpos >= ctot) break;
+          }
+          g.sync();
+          ncap = ctot - cpos;
+          cmn = ncap > 0 ? bits_to_d(I.x_hi[cpos]) : MF_INF;
+        } else if (ncap > 0) {
           int nc2 = 0;
           double mn = MF_INF;
           for (int base = 0; base < ncap; base += G::N) {
@@ -1989,15 +2039,7 @@ MF_UNROLL
         nt = nt2;
       }
       // slot counts of this class are back to zero (every member froze)
-      if (tiled) {
-#pragma unroll
-        for (int m = 0; m < kTile; ++m) {
-          if (g.lane() + m * G::N < n_tile0) res[tj[m]] = tr[m];
-          if (live & (1u << m)) cnt[tj[m]] = 0;
-        }
-      } else {
-        for (int jj = g.lane(); jj < nt; jj += G::N) cnt[tl[jj]] = 0;
-      }
+      for (int jj = g.lane(); jj < nt; jj += G::N) cnt[tl[jj]] = 0;
       g.sync();
     }
     s.classes += ncls;
