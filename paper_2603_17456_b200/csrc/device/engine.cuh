@@ -29,6 +29,9 @@
 
 namespace mfb {
 
+#ifndef MF_CAPSORT
+#define MF_CAPSORT 1  // A/B builds: -DMF_CAPSORT=0 keeps the per-round cap compaction
+#endif
 #define MF_INF (__builtin_huge_val())
 constexpr double kNoTime = -1.0;
 constexpr unsigned long long kNoSeq = ~0ull;
@@ -1108,8 +1111,10 @@ MF_UNROLL
       g.sync();
       const int nr = sorted_subset(I.s_ord + nd, SUB_NODL);
       ncls = group_classes(nd, nr, ncls);
+#ifndef MF_NO_AALO
     } else if (pol == POL_AALO) {
       ncls = decide_aalo(A);
+#endif
     } else {  // MFS arbitrate (rmlq.cpp:201-260)
       for (int p = g.lane(); p < A; p += G::N) {
         const int fid = I.a_fid[p];
@@ -1869,7 +1874,7 @@ MF_UNROLL
       MF_TOC(OUT_CY_SUB + 1, q1);
       if (nt > s.max_touch) s.max_touch = nt;
       // capped members sorted by cap once per class (rounds then walk a prefix)
-      const bool csorted = ncap > 1 && ncap <= kCapSort;
+      const bool csorted = MF_CAPSORT && ncap > 1 && ncap <= kCapSort;
       const int ctot = ncap;
       int cpos = 0;
       if (csorted) sort_caps(ncap);
@@ -2199,10 +2204,12 @@ MF_UNROLL
         I.r_open[r] = ropen - 1;
         I.r_lastfin[r] = smax(rlast, s.now);
       }
+#ifndef MF_NO_AALO
       if (I.p.policy == POL_AALO) {  // extension: attained bytes of the coflow
         const int ac = aalo_coflow(fid, b);
         if (ac >= 0) I.pl_att[ac] = dadd(I.pl_att[ac], size);
       }
+#endif
     }
     g.sync();
     if (pos >= 0) remove_active_at(fid, pos);

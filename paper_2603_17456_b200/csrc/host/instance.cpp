@@ -302,7 +302,8 @@ std::shared_ptr<TopoImage> build_topo_image(const Fabric& f, const Layout& lay) 
 std::shared_ptr<TopoImage> shared_topo_image(const Config& cfg) {
   std::string key;
   for (const char* k : {"topology.kind", "topology.hosts", "topology.nics_per_host",
-                        "topology.link_bytes_per_s", "topology.link_gbps", "cluster.prefill_units",
+                        "topology.link_bytes_per_s", "topology.link_gbps",
+                        "topology.oversubscription", "cluster.prefill_units",
                         "cluster.hosts_per_unit", "cluster.decode_hosts"})
     key += (cfg.has(k) ? "=" + cfg.str(k, "") : std::string("-")) + '\x1f';
   static std::mutex mu;

@@ -82,6 +82,23 @@ def test_oversub_host_engine_matches_oracle(emu, policy):
     assert not bits_equal(base.flow_finish, want.flow_finish)
 
 
+@needs_oracle
+def test_oversub_mixed_batch_matches_oracle(emu):
+    """one batch holding the same fabric with and without oversubscription: the
+    shared topology images and the deduplicated isolated-latency probes must
+    keep them apart"""
+    from paper_2603_17456_b200.native import DeviceBatch
+    texts = [oversub_fattree("fs", 1), oversub_fattree("fs", 2.0), cases.fattree_config("mfs"),
+             oversub_fattree("mfs", 3.0)]
+    b = DeviceBatch(0, emu)
+    for t in texts:
+        b.add_config(t)
+    b.prepare()
+    b.run(2)
+    for i, t in enumerate(texts):
+        assert diff(b.result(i, 2), ref.run_config(t, so=ref.ORACLE_SO)) == [], i
+
+
 @pytest.mark.gpu
 def test_oversub_device_matches_oracle(product):
     from paper_2603_17456_b200.native import DeviceBatch
