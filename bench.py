@@ -55,7 +55,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--instances", type=int, default=int(os.environ.get("MFSIM_BENCH_INSTANCES", 2368)),
+    ap.add_argument("--instances", type=int, default=int(os.environ.get("MFSIM_BENCH_INSTANCES", 3108)),
                     help="resident instances per rank")
     ap.add_argument("--slice-ms", type=float, default=1000.0,
                     help="device time per step (launch): every warp advances its instance until then")

@@ -30,7 +30,7 @@
 namespace mfb {
 
 #ifndef MF_CAPSORT
-#define MF_CAPSORT 1  // A/B builds: -DMF_CAPSORT=0 keeps the per-round cap compaction
+#define MF_CAPSORT 0  // 1: cap-sorted prefix walk (A/B: the per-class sort costs more than it saves)
 #endif
 #define MF_INF (__builtin_huge_val())
 constexpr double kNoTime = -1.0;
@@ -201,7 +201,10 @@ MF_FN bool ev_less(const Ev& x, const Ev& y) {
 // and the frozen-member bits in shared memory (engine_kernel.cu make_plan);
 // only the filling rounds are specialised on it, the rest of the engine is
 // one copy of code (instruction-cache footprint).
-template <class G>
+// kAalo: the Aalo extension's code is compiled in (a separate kernel instance,
+// launched only for batches holding aalo instances: the engine is
+// instruction-fetch bound and every code byte counts, profiles/r01_ab_engine_builds.txt)
+template <class G, bool kAalo = true>
 struct Engine {
   G g;
   Inst& I;  // per-warp copy (shared memory on the device), arrays possibly re-pointed
@@ -1111,10 +1114,8 @@ MF_UNROLL
       g.sync();
       const int nr = sorted_subset(I.s_ord + nd, SUB_NODL);
       ncls = group_classes(nd, nr, ncls);
-#ifndef MF_NO_AALO
-    } else if (pol == POL_AALO) {
+    } else if (kAalo && pol == POL_AALO) {
       ncls = decide_aalo(A);
-#endif
     } else {  // MFS arbitrate (rmlq.cpp:201-260)
       for (int p = g.lane(); p < A; p += G::N) {
         const int fid = I.a_fid[p];
@@ -2204,12 +2205,10 @@ MF_UNROLL
         I.r_open[r] = ropen - 1;
         I.r_lastfin[r] = smax(rlast, s.now);
       }
-#ifndef MF_NO_AALO
-      if (I.p.policy == POL_AALO) {  // extension: attained bytes of the coflow
+      if (kAalo && I.p.policy == POL_AALO) {  // extension: attained bytes of the coflow
         const int ac = aalo_coflow(fid, b);
         if (ac >= 0) I.pl_att[ac] = dadd(I.pl_att[ac], size);
       }
-#endif
     }
     g.sync();
     if (pos >= 0) remove_active_at(fid, pos);

@@ -57,6 +57,7 @@ __device__ __forceinline__ int sm_id() {
 // descending within a group; order[n + g] = offset of group g. A warp claims
 // from its SM's home group first -- SMs are mapped onto the groups in
 // proportion to their sizes -- then from the others.
+template <bool kAalo>
 __global__ void __launch_bounds__(32)
     mfsim_engine_kernel(const Inst* __restrict__ insts, const int* __restrict__ order, int n,
                         int groups, int nsm, int* __restrict__ next, SmemPlan plan,
@@ -137,7 +138,7 @@ __global__ void __launch_bounds__(32)
     }
     slots_on_chip = __shfl_sync(0xffffffffu, slots_on_chip, 0);
     __syncwarp();
-    Engine<WarpLanes> eng(*d, slots_on_chip);
+    Engine<WarpLanes, kAalo> eng(*d, slots_on_chip);
     const bool done = eng.run(budget, deadline);
     if (done && lane == 0) atomicSub(remaining, 1);
     __syncwarp();
@@ -165,9 +166,9 @@ class CudaBackend final : public Backend {
     ck(cudaMalloc(&counter_, (1 + kMaxGroups) * sizeof(int)), "cudaMalloc counter");
     ck(cudaMallocHost(&remain_host_, sizeof(int)), "cudaMallocHost");
     ck(cudaDeviceGetAttribute(&sms_, cudaDevAttrMultiProcessorCount, device), "attr");
-    ck(cudaFuncSetAttribute(mfb::mfsim_engine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            200 * 1024),
-       "smem attr");
+    for (auto k : {mfb::mfsim_engine_kernel<false>, mfb::mfsim_engine_kernel<true>})
+      ck(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024),
+         "smem attr");
     // deep per-warp call chains (noinline handlers) need more than the default
     ck(cudaDeviceSetLimit(cudaLimitStackSize, 4096), "stack limit");
   }
@@ -201,7 +202,9 @@ class CudaBackend final : public Backend {
               long long budget, long long slice_ns) override {
     const mfb::SmemPlan plan = mfb::make_plan(hint.nlinks);
     int per_sm = 0;
-    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mfb::mfsim_engine_kernel, 32,
+    // the lean kernel unless the batch holds Aalo instances (extension code compiled out)
+    auto kern = hint.aalo ? mfb::mfsim_engine_kernel<true> : mfb::mfsim_engine_kernel<false>;
+    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32,
                                                      plan.bytes),
        "occupancy");
     if (per_sm < 1) per_sm = 1;
@@ -209,7 +212,7 @@ class CudaBackend final : public Backend {
     if (n < grid) grid = n > 0 ? n : 1;
     ck(cudaMemsetAsync(counter_ + 1, 0, sizeof(int) * kMaxGroups, stream_), "memset");
     ck(cudaEventRecord(e0_, stream_), "event");
-    mfb::mfsim_engine_kernel<<<grid, 32, plan.bytes, stream_>>>(
+    kern<<<grid, 32, plan.bytes, stream_>>>(
         d, order, n, hint.groups, sms_, counter_ + 1, plan, budget, slice_ns, counter_);
     ck(cudaGetLastError(), "launch");
     ck(cudaEventRecord(e1_, stream_), "event");

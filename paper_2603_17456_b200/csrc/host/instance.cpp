@@ -951,6 +951,7 @@ void Batch::pack() {
       for (const Inst& d : desc_) {
         hint_.rmax = std::max(hint_.rmax, d.rmax);
         hint_.nlinks = std::max(hint_.nlinks, d.nlinks);
+        hint_.aalo = hint_.aalo || d.p.policy == mfb::POL_AALO;
       }
       in_bytes_ = c.in.off;
       st_bytes_ = c.st.off;

@@ -32,6 +32,7 @@ struct LaunchHint {
   int rmax = 1;    // longest route of any instance
   int nlinks = 1;  // most links of any instance
   int groups = 1;  // claim groups (one per policy): order[n .. n+groups] holds their offsets
+  bool aalo = false;  // some instance runs the Aalo extension (kernel variant with its code)
 };
 constexpr int kMaxGroups = 8;
 
