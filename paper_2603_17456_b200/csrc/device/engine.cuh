@@ -29,9 +29,6 @@
 
 namespace mfb {
 
-#ifndef MF_CAPSORT
-#define MF_CAPSORT 0  // 1: cap-sorted prefix walk (A/B: the per-class sort costs more than it saves)
-#endif
 #define MF_INF (__builtin_huge_val())
 constexpr double kNoTime = -1.0;
 constexpr unsigned long long kNoSeq = ~0ull;
@@ -1635,98 +1632,6 @@ MF_UNROLL
   }
 
   // class filling with the shared class rate over the link slots
-  // Ascending sort of the capped entries (x_hi = cap bits, x_lo = active
-  // position) of one class, n <= kCapSort: a bitonic network over registers
-  // (8 entries per lane; lane-crossing stages by shuffle, register-crossing
-  // stages by static pairs). Caps are >= 0, so their bit patterns order like
-  // the values; equal caps may come out in any order (they freeze together).
-  static constexpr int kCapSort = 8 * G::N;
-  MF_FN static bool kv_gt(unsigned long long ha, unsigned la, unsigned long long hb, unsigned lb) {
-    return ha > hb || (ha == hb && la > lb);
-  }
-  MF_NOINLINE void sort_caps(int n) {
-    unsigned long long* __restrict__ xh = I.x_hi;
-    unsigned long long* __restrict__ xl = I.x_lo;
-    if (G::N == 1) {  // serial build: insertion sort
-      for (int i = 1; i < n; ++i) {
-        const unsigned long long h = xh[i], l = xl[i];
-        int j = i - 1;
-        while (j >= 0 && kv_gt((unsigned long long)xh[j], (unsigned)xl[j], h, (unsigned)l)) {
-          xh[j + 1] = xh[j];
-          xl[j + 1] = xl[j];
-          --j;
-        }
-        xh[j + 1] = h;
-        xl[j + 1] = l;
-      }
-      return;
-    }
-    constexpr int E = 8;
-    int n2 = G::N;
-    while (n2 < n) n2 <<= 1;
-    const int nm = n2 / G::N;
-    unsigned long long h[E];
-    unsigned lo[E];
-#pragma unroll
-    for (int m = 0; m < E; ++m) {
-      const int i = m * G::N + g.lane();
-      h[m] = i < n ? xh[i] : ~0ull;
-      lo[m] = i < n ? (unsigned)xl[i] : ~0u;
-    }
-#define MF_CS(a, b)                                                   \
-  if ((b) < nm) {                                                      \
-    const bool up = (((a)*G::N + g.lane()) & k) == 0;                  \
-    if (kv_gt(h[a], lo[a], h[b], lo[b]) == up) {                       \
-      const unsigned long long th = h[a];                              \
-      const unsigned tl_ = lo[a];                                      \
-      h[a] = h[b];                                                     \
-      lo[a] = lo[b];                                                   \
-      h[b] = th;                                                       \
-      lo[b] = tl_;                                                     \
-    }                                                                  \
-  }
-    for (int k = 2; k <= n2; k <<= 1) {
-      for (int j = k >> 1; j > 0; j >>= 1) {
-        if (j >= G::N) {
-          const int jm = j / G::N;
-          if (jm == 1) {
-            MF_CS(0, 1) MF_CS(2, 3) MF_CS(4, 5) MF_CS(6, 7)
-          } else if (jm == 2) {
-            MF_CS(0, 2) MF_CS(1, 3) MF_CS(4, 6) MF_CS(5, 7)
-          } else {
-            MF_CS(0, 4) MF_CS(1, 5) MF_CS(2, 6) MF_CS(3, 7)
-          }
-        } else {
-          const bool lower = (g.lane() & j) == 0;
-#pragma unroll
-          for (int m = 0; m < E; ++m) {
-            if (m < nm) {
-              const unsigned long long ph = g.shfl_xor(h[m], j);
-              const unsigned pl = (unsigned)g.shfl_xor((int)lo[m], j);
-              const bool up = ((m * G::N + g.lane()) & k) == 0;
-              const bool take = (lower == up) ? kv_gt(h[m], lo[m], ph, pl) : kv_gt(ph, pl, h[m], lo[m]);
-              if (take) {
-                h[m] = ph;
-                lo[m] = pl;
-              }
-            }
-          }
-        }
-      }
-    }
-#undef MF_CS
-    g.sync();
-#pragma unroll
-    for (int m = 0; m < E; ++m) {
-      const int i = m * G::N + g.lane();
-      if (m < nm && i < n) {
-        xh[i] = h[m];
-        xl[i] = lo[m];
-      }
-    }
-    g.sync();
-  }
-
   template <bool kLinksOnChip>
   MF_NOINLINE void allocate_slots(int ncls, bool has_caps) {
     const int A = s.n_active;
@@ -1874,11 +1779,22 @@ MF_UNROLL
       }
       MF_TOC(OUT_CY_SUB + 1, q1);
       if (nt > s.max_touch) s.max_touch = nt;
-      // capped members sorted by cap once per class (rounds then walk a prefix)
-      const bool csorted = MF_CAPSORT && ncap > 1 && ncap <= kCapSort;
+      // capped members stay where the count pass put them; lane l owns entries
+      // l, l+N, ... and keeps the minimum cap of its unfrozen ones (value,
+      // entry, member). A round rescans only lanes whose minimum got frozen
+      // through a link or became freezable: R >= cap - 1e-12 max(1, cap) is
+      // monotone in cap, so a lane whose minimum stays is untouched.
       const int ctot = ncap;
-      int cpos = 0;
-      if (csorted) sort_caps(ncap);
+      double lmin = MF_INF;
+      int lpos = -1, lp = -1;
+      for (int i = g.lane(); i < ctot; i += G::N) {
+        const double cp = bits_to_d(I.x_hi[i]);
+        if (cp < lmin) {
+          lmin = cp;
+          lpos = i;
+        }
+      }
+      if (lpos >= 0) lp = (int)I.x_lo[lpos];
       int nu = n;
       double R = 0.0;
       while (nu > 0) {
@@ -1961,73 +1877,40 @@ MF_UNROLL
         // cap freezes (the same rate R, so the order against the link freezes
         // is immaterial): drop frozen entries, freeze cap - eps <= R, and take
         // the minimum cap of the survivors for the next round
-        if (ncap > 0 && csorted) {
-          // cap-sorted entries: R >= cap - 1e-12 max(1, cap) holds on a prefix
-          // (the threshold is increasing in cap), so the pass is a pointer
-          // walk; entries frozen through a link are stepped over
-          for (;;) {
-            const int i = cpos + g.lane();
-            bool pass = false, fz = false;
-            int p = 0;
-            if (i < ctot) {
-              p = (int)I.x_lo[i];
-              const bool was = (frz[p >> 5] & (1u << (p & 31))) != 0u;
-              const double cp = bits_to_d(I.x_hi[i]);
-              fz = !was && R >= dsub(cp, dmul(1e-12, smax(1.0, cp)));
-              pass = was || fz;
-            }
-            const unsigned stop = g.ballot(!pass);
-            const int adv = stop ? ctz32(stop) : G::N;
-            if (fz && g.lane() < adv) {
-              g.atomic_or(&frz[p >> 5], 1u << (p & 31));
-              rate[p] = R;
-              const int rn = arnp[p];
-              for (int k = 0; k < rn; ++k) g.atomic_add(&cnt[asl[p * RM + k]], -1);
-              ++got;
-            }
-            cpos = cpos + adv < ctot ? cpos + adv : ctot;
-            if (stop || cpos >= ctot) break;
-          }
-          g.sync();
-          ncap = ctot - cpos;
-          cmn = ncap > 0 ? bits_to_d(I.x_hi[cpos]) : MF_INF;
-        } else if (ncap > 0) {
-          int nc2 = 0;
-          double mn = MF_INF;
-          for (int base = 0; base < ncap; base += G::N) {
-            const int i = base + g.lane();
-            bool keep = false, fz = false;
-            int p = 0;
-            double cp = 0.0;
-            if (i < ncap) {
-              p = (int)I.x_lo[i];
-              if (!(frz[p >> 5] & (1u << (p & 31)))) {
-                cp = bits_to_d(I.x_hi[i]);
-                fz = R >= dsub(cp, dmul(1e-12, smax(1.0, cp)));
-                keep = !fz;
+        if (ncap > 0) {
+          bool need = false;
+          if (lpos >= 0)
+            need = (frz[lp >> 5] & (1u << (lp & 31))) != 0u ||
+                   R >= dsub(lmin, dmul(1e-12, smax(1.0, lmin)));
+          if (g.any(need)) {
+            if (need) {
+              double mn = MF_INF;
+              int mpos = -1;
+              for (int i = g.lane(); i < ctot; i += G::N) {
+                const int p = (int)I.x_lo[i];
+                if (frz[p >> 5] & (1u << (p & 31))) continue;  // frozen (link or earlier cap)
+                const double cp = bits_to_d(I.x_hi[i]);
+                if (R >= dsub(cp, dmul(1e-12, smax(1.0, cp)))) {
+                  g.atomic_or(&frz[p >> 5], 1u << (p & 31));  // entries are per member: no race
+                  rate[p] = R;
+                  const int rn = arnp[p];
+                  for (int k = 0; k < rn; ++k) g.atomic_add(&cnt[asl[p * RM + k]], -1);
+                  ++got;
+                  continue;
+                }
+                if (cp < mn) {
+                  mn = cp;
+                  mpos = i;
+                }
               }
+              lmin = mn;
+              lpos = mpos;
+              lp = mpos >= 0 ? (int)I.x_lo[mpos] : -1;
             }
-            g.sync();  // every lane has read its entry before the in-place compaction
-            if (fz) {
-              g.atomic_or(&frz[p >> 5], 1u << (p & 31));
-              rate[p] = R;
-              const int rn = arnp[p];
-              for (int k = 0; k < rn; ++k) g.atomic_add(&cnt[asl[p * RM + k]], -1);
-              ++got;
-            }
-            const unsigned mk = g.ballot(keep);
-            if (keep) {
-              const int slot = nc2 + popc32(mk & g.lanemask_lt());
-              I.x_hi[slot] = dbits(cp);
-              I.x_lo[slot] = (unsigned long long)p;
-              mn = smin(mn, cp);
-            }
-            nc2 += popc32(mk);
+            g.sync();
           }
-          mn = g.min_nonneg(mn);  // stored caps are smax(0, cap) >= 0
-          g.sync();
-          ncap = nc2;
-          cmn = mn;
+          cmn = g.min_nonneg(lmin);  // stored caps are smax(0, cap) >= 0
+          ncap = cmn < MF_INF ? 1 : 0;  // only "any capped member left" is used
         }
         int frozen = 0;
         if (ns > 0 || has_caps) {
