@@ -1779,22 +1779,6 @@ MF_UNROLL
       }
       MF_TOC(OUT_CY_SUB + 1, q1);
       if (nt > s.max_touch) s.max_touch = nt;
-      // capped members stay where the count pass put them; lane l owns entries
-      // l, l+N, ... and keeps the minimum cap of its unfrozen ones (value,
-      // entry, member). A round rescans only lanes whose minimum got frozen
-      // through a link or became freezable: R >= cap - 1e-12 max(1, cap) is
-      // monotone in cap, so a lane whose minimum stays is untouched.
-      const int ctot = ncap;
-      double lmin = MF_INF;
-      int lpos = -1, lp = -1;
-      for (int i = g.lane(); i < ctot; i += G::N) {
-        const double cp = bits_to_d(I.x_hi[i]);
-        if (cp < lmin) {
-          lmin = cp;
-          lpos = i;
-        }
-      }
-      if (lpos >= 0) lp = (int)I.x_lo[lpos];
       int nu = n;
       double R = 0.0;
       while (nu > 0) {
@@ -1878,39 +1862,42 @@ MF_UNROLL
         // is immaterial): drop frozen entries, freeze cap - eps <= R, and take
         // the minimum cap of the survivors for the next round
         if (ncap > 0) {
-          bool need = false;
-          if (lpos >= 0)
-            need = (frz[lp >> 5] & (1u << (lp & 31))) != 0u ||
-                   R >= dsub(lmin, dmul(1e-12, smax(1.0, lmin)));
-          if (g.any(need)) {
-            if (need) {
-              double mn = MF_INF;
-              int mpos = -1;
-              for (int i = g.lane(); i < ctot; i += G::N) {
-                const int p = (int)I.x_lo[i];
-                if (frz[p >> 5] & (1u << (p & 31))) continue;  // frozen (link or earlier cap)
-                const double cp = bits_to_d(I.x_hi[i]);
-                if (R >= dsub(cp, dmul(1e-12, smax(1.0, cp)))) {
-                  g.atomic_or(&frz[p >> 5], 1u << (p & 31));  // entries are per member: no race
-                  rate[p] = R;
-                  const int rn = arnp[p];
-                  for (int k = 0; k < rn; ++k) g.atomic_add(&cnt[asl[p * RM + k]], -1);
-                  ++got;
-                  continue;
-                }
-                if (cp < mn) {
-                  mn = cp;
-                  mpos = i;
-                }
+          int nc2 = 0;
+          double mn = MF_INF;
+          for (int base = 0; base < ncap; base += G::N) {
+            const int i = base + g.lane();
+            bool keep = false, fz = false;
+            int p = 0;
+            double cp = 0.0;
+            if (i < ncap) {
+              p = (int)I.x_lo[i];
+              if (!(frz[p >> 5] & (1u << (p & 31)))) {
+                cp = bits_to_d(I.x_hi[i]);
+                fz = R >= dsub(cp, dmul(1e-12, smax(1.0, cp)));
+                keep = !fz;
               }
-              lmin = mn;
-              lpos = mpos;
-              lp = mpos >= 0 ? (int)I.x_lo[mpos] : -1;
             }
-            g.sync();
+            g.sync();  // every lane has read its entry before the in-place compaction
+            if (fz) {
+              g.atomic_or(&frz[p >> 5], 1u << (p & 31));
+              rate[p] = R;
+              const int rn = arnp[p];
+              for (int k = 0; k < rn; ++k) g.atomic_add(&cnt[asl[p * RM + k]], -1);
+              ++got;
+            }
+            const unsigned mk = g.ballot(keep);
+            if (keep) {
+              const int slot = nc2 + popc32(mk & g.lanemask_lt());
+              I.x_hi[slot] = dbits(cp);
+              I.x_lo[slot] = (unsigned long long)p;
+              mn = smin(mn, cp);
+            }
+            nc2 += popc32(mk);
           }
-          cmn = g.min_nonneg(lmin);  // stored caps are smax(0, cap) >= 0
-          ncap = cmn < MF_INF ? 1 : 0;  // only "any capped member left" is used
+          mn = g.min_nonneg(mn);  // stored caps are smax(0, cap) >= 0
+          g.sync();
+          ncap = nc2;
+          cmn = mn;
         }
         int frozen = 0;
         if (ns > 0 || has_caps) {
