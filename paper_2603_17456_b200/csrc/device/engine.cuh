@@ -1632,6 +1632,24 @@ MF_UNROLL
   }
 
   // class filling with the shared class rate over the link slots
+  // cnt[slot] += v over one member's route slots. ILP build (-DMF_ROUTE_ILP):
+  // the slot ids are loaded together, then the (non-returning) atomics issue
+  // back to back, instead of a load -> atomic chain per link.
+  MF_FN void route_slots_add(int* __restrict__ cnt, const unsigned short* __restrict__ sl, int rn, int v) const {
+#if defined(MF_ROUTE_ILP)
+    if (rn <= 6) {
+      int j[6];
+#pragma unroll
+      for (int k = 0; k < 6; ++k) j[k] = k < rn ? sl[k] : -1;
+#pragma unroll
+      for (int k = 0; k < 6; ++k)
+        if (j[k] >= 0) g.atomic_add(&cnt[j[k]], v);
+      return;
+    }
+#endif
+    for (int k = 0; k < rn; ++k) g.atomic_add(&cnt[sl[k]], v);
+  }
+
   template <bool kLinksOnChip>
   MF_NOINLINE void allocate_slots(int ncls, bool has_caps) {
     const int A = s.n_active;
@@ -1853,7 +1871,7 @@ MF_UNROLL
             if ((frz[p >> 5] & bit) || (g.atomic_or(&frz[p >> 5], bit) & bit)) continue;
             rate[p] = R;
             const int rn = arnp[p];
-            for (int k = 0; k < rn; ++k) g.atomic_add(&cnt[asl[p * RM + k]], -1);
+            route_slots_add(cnt, asl + p * RM, rn, -1);
             ++got;
           }
         }
@@ -1882,7 +1900,7 @@ MF_UNROLL
               g.atomic_or(&frz[p >> 5], 1u << (p & 31));
               rate[p] = R;
               const int rn = arnp[p];
-              for (int k = 0; k < rn; ++k) g.atomic_add(&cnt[asl[p * RM + k]], -1);
+              route_slots_add(cnt, asl + p * RM, rn, -1);
               ++got;
             }
             const unsigned mk = g.ballot(keep);

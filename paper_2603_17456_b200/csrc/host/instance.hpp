@@ -26,7 +26,10 @@ namespace mfh {
 constexpr int kDefaultActive = 1024;  // first-attempt active-set capacity
 constexpr int kSmemEvents = 64;       // event pool staged on chip
 constexpr int kSmemLinks = 1024;      // link -> slot map staged on chip
-constexpr int kSmemSlots = 256;       // per-slot filling state staged on chip
+#ifndef MF_SMEM_SLOTS
+#define MF_SMEM_SLOTS 256
+#endif
+constexpr int kSmemSlots = MF_SMEM_SLOTS;       // per-slot filling state staged on chip
 
 struct LaunchHint {
   int rmax = 1;    // longest route of any instance
