@@ -55,8 +55,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--instances", type=int, default=int(os.environ.get("MFSIM_BENCH_INSTANCES", 3108)),
-                    help="resident instances per rank")
+    ap.add_argument("--instances", type=int, default=int(os.environ.get("MFSIM_BENCH_INSTANCES", 0)),
+                    help="resident instances per rank (0: WARPS_PER_SM x SMs, bounded by free HBM)")
     ap.add_argument("--slice-ms", type=float, default=1000.0,
                     help="device time per step (launch): every warp advances its instance until then")
     ap.add_argument("--requests", type=int, default=2000, help="requests per instance (configs[3]: 2000)")
@@ -111,6 +111,19 @@ class Clocks:
         reasons = sorted({names[i] for r in load for i in range(4) if r[3 + i].lower() == "active"})
         return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": float(rows[0][1]), "reasons": reasons,
                 "samples": len(load)}
+
+
+WARPS_PER_SM = 28          # resident instances per SM (the shared-memory plan allows 29)
+INSTANCE_BYTES = 38.0e6    # device arena of one configs[3] instance (measured 37.3 MB)
+
+
+def resident_instances(device: int) -> int:
+    """one warp-resident instance per warp slot, as many as free HBM holds"""
+    import torch
+    props = torch.cuda.get_device_properties(device)
+    free, _ = torch.cuda.mem_get_info(device)
+    by_mem = int((free - 8e9) / INSTANCE_BYTES)
+    return max(148, min(WARPS_PER_SM * props.multi_processor_count, by_mem))
 
 
 def cells_for(rank: int, world: int, n: int, step_offset: int = 0):
@@ -175,6 +188,8 @@ def cpu_reference(cells, requests, budget_s, lib_cfg):
 def reference_arm(args, rank, world):
     if rank != 0:
         return
+    if args.instances <= 0:
+        args.instances = WARPS_PER_SM * 148
     from paper_2603_17456_b200 import sweep
 
     def cfg_text(c):
@@ -183,7 +198,7 @@ def reference_arm(args, rank, world):
     def sweep_text(c, n):
         return sweep.sweep_config(c, requests=n, lib=_emu_or_product())
 
-    cells = cells_for(0, 1, max(args.instances, 64))
+    cells = cells_for(0, 1, args.instances if args.instances > 0 else WARPS_PER_SM * 148)
     # one bounded sample of the same cells, shared by the K steps: instances are
     # submitted for ~cpu_sample_s seconds and run to completion on all cores
     r = cpu_reference(cells, args.requests, args.cpu_sample_s, cfg_text)
@@ -251,6 +266,8 @@ def main():
     lib = product()
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
+    if args.instances <= 0:
+        args.instances = resident_instances(local)
     cells = cells_for(rank, world, args.instances)
     t0 = time.perf_counter()
     batch = DeviceBatch(local, lib, stream=stream.cuda_stream)
