@@ -136,7 +136,13 @@ def cells_for(rank: int, world: int, n: int, step_offset: int = 0):
 
     from paper_2603_17456_b200 import sweep
 
-    allc = sweep.sweep_cells()
+    # 64 seeds = 11,200 cells; runs that need more distinct instances (weak
+    # scaling to 8 GPUs x ~4k resident instances) continue with seeds 65, 66, ...
+    # instead of re-simulating cells
+    need = (step_offset * world + world) * n
+    per_seed = len(sweep.LOADS) * len(sweep.SLO_SCALES) * len(sweep.POLICIES)
+    seeds = max(64, -(-need // per_seed))
+    allc = sweep.sweep_cells(seeds=range(1, seeds + 1))
     rng = random.Random(2603)
     blocks = {}
     for c in allc:
@@ -237,7 +243,8 @@ def workload_config(args):
     return {
         "workload": "configs[3] sweep: ft128 fat-tree (128 hosts x 8 NICs, k=8, 768 links), "
                     "16 units x 4 hosts + 64 decode, cells = load {0.3..0.9} x SLO {1..5} x "
-                    "seed {1..64} x policy {fs,sjf,edf,karuna,mfs}",
+                    "seed {1..64} x policy {fs,sjf,edf,karuna,mfs} (seeds 65.. when ranks x resident "
+                    "instances exceed the 11,200 cells: every instance distinct)",
         "instances_per_rank": args.instances,
         "step": f"one launch = {args.slice_ms:g} ms of device time per warp (time-sliced, "
                 "instances suspend to HBM and resume exactly)",
