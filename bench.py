@@ -113,7 +113,7 @@ class Clocks:
                 "samples": len(load)}
 
 
-WARPS_PER_SM = 28          # resident instances per SM (the shared-memory plan allows 29)
+WARPS_PER_SM = 32          # resident instances per SM (registers and the shared-memory plan allow 32)
 INSTANCE_BYTES = 38.0e6    # device arena of one configs[3] instance (measured 37.3 MB)
 
 

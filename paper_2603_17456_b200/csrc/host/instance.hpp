@@ -27,10 +27,11 @@ constexpr int kDefaultActive = 1024;  // first-attempt active-set capacity
 constexpr int kSmemEvents = 64;       // event pool staged on chip
 constexpr int kSmemLinks = 1024;      // link -> slot map staged on chip
 #ifndef MF_SMEM_SLOTS
-#define MF_SMEM_SLOTS 128
+#define MF_SMEM_SLOTS 96
 #endif
-// per-slot filling state staged on chip: 128 slots fit 29 warps per SM and
-// cost nothing against 256 (A/B, profiles/r01_ab_engine_builds.txt call 9)
+// per-slot filling state staged on chip: 96 slots let 32 warps per SM stay
+// resident (the 64-register limit) and cost nothing per warp against 128 or
+// 256 (A/B, profiles/r01_ab_engine_builds.txt calls 9 and 11)
 constexpr int kSmemSlots = MF_SMEM_SLOTS;
 
 struct LaunchHint {
