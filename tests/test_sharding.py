@@ -75,3 +75,15 @@ def test_two_rank_sharding_matches_single_rank():
     b.run(0)
     assert [(b.stats(i).events, b.stats(i).slo_met) for i in range(len(cells))] == \
         [(x[1], x[2]) for x in flat]
+
+
+def test_cells_distinct_at_eight_ranks():
+    """weak scaling never re-simulates a cell: 8 ranks x 4736 resident instances
+    exceed the 11,200 cells of 64 seeds and continue with seeds 65, 66, ..."""
+    import sys
+    sys.path.insert(0, ROOT)
+    import bench
+    allr = [c for r in range(8) for c in bench.cells_for(r, 8, 4736)]
+    assert len(allr) == len(set(allr)) == 8 * 4736
+    assert bench.cells_for(0, 1, 4736) == bench.cells_for(0, 8, 4736)  # rank 0 is stable
+    assert max(c[2] for c in allr) > 64
