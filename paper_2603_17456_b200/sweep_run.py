@@ -20,6 +20,16 @@ cell's summary.
   python -m paper_2603_17456_b200.sweep_run --config C --policies fs,mfs \
       --rates 1,2 --seeds 1,2,3 --out DIR
   torchrun --nproc-per-node 8 --master-addr 127.0.0.1 -m paper_2603_17456_b200.sweep_run ...
+
+Beyond simsweep, an SLO-multiplier axis (`--slo-multipliers 1,2,3`, sets
+`workload.slo_multiplier`) and an offered-load axis (`--loads 0.3,0.5`, each
+rho mapped to `workload.rate_rps` by `sweep.rate_for_load` on the base config)
+give BASELINE configs[3]'s grid; `--grid configs3` is that whole grid (ft128,
+2000 requests, rho 0.3..0.9 x SLO 1..5 x seeds 1..64 x 5 policies = 11,200
+cells). With the SLO axis the cells are (policy, rate, seed, slo) and
+sweep.csv gains a `slo_multiplier` column after `seed`; without it every
+output is simsweep's, byte for byte. A rank's share runs in device batches of
+at most `--batch-cap` instances (default: what free HBM holds).
 """
 from __future__ import annotations
 
@@ -43,13 +53,39 @@ def split_list(s: str):
     return [x for x in s.split(",") if x]
 
 
-def sweep_cells(policies, rates, seeds):
-    return [(p, r, s) for p in policies for r in rates for s in seeds]
+def sweep_cells(policies, rates, seeds, slos=None):
+    """simsweep order (policy-major, then rate, then seed); the SLO-multiplier
+    axis, when given, is innermost"""
+    if not slos:
+        return [(p, r, s) for p in policies for r in rates for s in seeds]
+    return [(p, r, s, m) for p in policies for r in rates for s in seeds for m in slos]
 
 
 def cell_dir(out: str, cell) -> str:
-    p, r, s = cell
-    return os.path.join(out, p, "rate_" + r, "seed_" + s)
+    d = os.path.join(out, cell[0], "rate_" + cell[1], "seed_" + cell[2])
+    return os.path.join(d, "slo_" + cell[3]) if len(cell) > 3 else d
+
+
+def cell_key(cell) -> str:
+    return "/".join([cell[0], "rate_" + cell[1], "seed_" + cell[2]] +
+                    (["slo_" + cell[3]] if len(cell) > 3 else []))
+
+
+def csv_header(slo_axis: bool) -> str:
+    if not slo_axis:
+        return CSV_HEADER
+    return CSV_HEADER.replace("seed,", "seed,slo_multiplier,", 1)
+
+
+def parse_config_text(text: str) -> dict:
+    """`section.key = value` lines (config.cpp's format; '#' comments) -> dict"""
+    d = {}
+    for line in text.splitlines():
+        line = line.split("#", 1)[0].strip()
+        if "=" in line:
+            k, v = line.split("=", 1)
+            d[k.strip()] = v.strip()
+    return d
 
 
 def shard(cells, world: int, cost=None):
@@ -76,8 +112,7 @@ def json_token(summary: str, key: str) -> str:
 
 
 def csv_row(cell, summary: str) -> str:
-    p, r, s = cell
-    return ",".join([p, r, s] + [json_token(summary, k) for k in CSV_KEYS]) + "\n"
+    return ",".join(list(cell) + [json_token(summary, k) for k in CSV_KEYS]) + "\n"
 
 
 def ttft_and_flags(res):
@@ -130,8 +165,14 @@ def main(argv=None, lib=None, backend=None):
     ap.add_argument("--policies", default="fs,sjf,edf,karuna,mfs")
     ap.add_argument("--rates", default="1")
     ap.add_argument("--seeds", default="1")
+    ap.add_argument("--slo-multipliers", default="", help="SLO-multiplier axis (workload.slo_multiplier)")
+    ap.add_argument("--loads", default="", help="offered-load axis rho (replaces --rates)")
+    ap.add_argument("--grid", default="", choices=["", "configs3"],
+                    help="configs3: BASELINE configs[3]'s whole 11,200-cell grid")
+    ap.add_argument("--batch-cap", type=int, default=0, help="max instances per device batch (0: all)")
     ap.add_argument("--out", default="sweep_out")
     ap.add_argument("--no-reports", action="store_true", help="skip per-cell requests.csv/summary.json")
+    ap.add_argument("--no-ttft-npz", action="store_true", help="gather, check, but do not write ttft.npz")
     a = ap.parse_args(argv)
 
     import torch
@@ -154,25 +195,47 @@ def main(argv=None, lib=None, backend=None):
         dist.init_process_group(backend, rank=rank, world_size=world)
 
     base = open(a.config).read() if a.config else ""
-    cells = sweep_cells(split_list(a.policies), split_list(a.rates), split_list(a.seeds))
+    if a.grid == "configs3":
+        from . import sweep
+        base = sweep.text(dict(sweep.FT128, **{"workload.request_count": 2000}))
+        a.policies = ",".join(sweep.POLICIES)
+        a.loads = ",".join(str(x) for x in sweep.LOADS)
+        a.slo_multipliers = ",".join(str(x) for x in sweep.SLO_SCALES)
+        a.seeds = ",".join(str(x) for x in range(1, 65))
+        a.batch_cap = a.batch_cap or 4000
+    rates = split_list(a.rates)
+    if a.loads:  # rho -> per-unit request rate on this base config (sweep.rate_for_load)
+        from . import sweep
+        cfg = parse_config_text(base)
+        rates = [repr(sweep.rate_for_load(float(x), cfg, lib)) for x in split_list(a.loads)]
+    slos = split_list(a.slo_multipliers)
+    cells = sweep_cells(split_list(a.policies), rates, split_list(a.seeds), slos)
     owner = shard(cells, world)
     mine = [i for i in range(len(cells)) if owner[i] == rank]
 
     def text(cell):
-        p, r, s = cell
         c = Config(base, lib)
-        c.set("policy", p).set("workload.rate_rps", r).set("sim.seed", s)
+        c.set("policy", cell[0]).set("workload.rate_rps", cell[1]).set("sim.seed", cell[2])
+        if len(cell) > 3:
+            c.set("workload.slo_multiplier", cell[3])
         return c
 
+    import time
     results = []
-    if mine:
-        batch, results = run_cells([text(cells[i]) for i in mine], lib, device=local)
+    cap = a.batch_cap if a.batch_cap > 0 else max(len(mine), 1)
+    t0 = time.time()
+    for c0 in range(0, len(mine), cap):
+        part = mine[c0:c0 + cap]
+        batch, res = run_cells([text(cells[i]) for i in part], lib, device=local)
+        print(f"rank {rank}: batch of {len(part)} cells, {sum(r[3].events for r in res)} events, "
+              f"{time.time() - t0:.1f} s since start", flush=True)
         if not a.no_reports:
-            for k, i in enumerate(mine):
+            for k, i in enumerate(part):
                 d = cell_dir(a.out, cells[i])
                 os.makedirs(d, exist_ok=True)
                 lib.check(lib.lib.mfsim_dev_write_report(batch.h, k, d.encode()))
         del batch
+        results.extend(res)
 
     # final gather of per-request TTFT + SLO flags (and the summaries) to rank 0
     idx = np.array(mine, np.int64)
@@ -201,7 +264,7 @@ def main(argv=None, lib=None, backend=None):
                 off += n
         assert sorted(per_cell) == list(range(len(cells))), "gather lost cells"
         os.makedirs(a.out, exist_ok=True)
-        rows = [CSV_HEADER]
+        rows = [csv_header(bool(slos))]
         for i, cell in enumerate(cells):
             summary = summaries[i]
             tt, fl = per_cell[i]
@@ -220,13 +283,14 @@ def main(argv=None, lib=None, backend=None):
             rows.append(csv_row(cell, summary))
         with open(os.path.join(a.out, "sweep.csv"), "w", newline="") as f:
             f.write("".join(rows))
-        np.savez_compressed(os.path.join(a.out, "ttft.npz"),
-                            **{f"{p}/rate_{r}/seed_{s}/ttft": per_cell[i][0]
-                               for i, (p, r, s) in enumerate(cells)},
-                            **{f"{p}/rate_{r}/seed_{s}/slo_met": per_cell[i][1]
-                               for i, (p, r, s) in enumerate(cells)})
-        for p, r, s in cells:
-            print(f"done {p} rate={r} seed={s}")
+        if not a.no_ttft_npz:
+            np.savez_compressed(os.path.join(a.out, "ttft.npz"),
+                                **{cell_key(c) + "/ttft": per_cell[i][0] for i, c in enumerate(cells)},
+                                **{cell_key(c) + "/slo_met": per_cell[i][1] for i, c in enumerate(cells)})
+        if len(cells) <= 1000:
+            for c in cells:
+                print("done " + cell_key(c))
+        print(f"sweep: {len(cells)} cells on {world} rank(s), sweep.csv written", flush=True)
     if init_here:
         dist.barrier()
         dist.destroy_process_group()

@@ -123,3 +123,34 @@ def test_sweep_on_device_matches_reference_simsweep(tmp_path):
         os.environ.pop(k, None)
     sweep_run.main(argv + ["--out", out])
     _check(out, conf)
+
+
+def test_slo_axis_and_loads_on_emulation(tmp_path):
+    """SLO-multiplier and offered-load axes (configs[3]'s grid) with batch
+    chunking: every row equals the reference run of the same cell"""
+    from oracle import ref
+    if not ref.available():
+        pytest.skip("reference library (oracle/_ref) not built")
+    from paper_2603_17456_b200 import sweep, sweep_run
+    from paper_2603_17456_b200.native import Native
+    emu = Native(os.path.join(ROOT, "build", "libmfsim_emu.so"))
+    conf = _conf(str(tmp_path))
+    out = str(tmp_path / "o")
+    sweep_run.main(["--config", conf, "--policies", "fs,mfs", "--loads", "0.4,0.8",
+                    "--seeds", "3", "--slo-multipliers", "1,4", "--batch-cap", "3",
+                    "--no-reports", "--out", out], lib=emu, backend="gloo")
+    base = open(conf).read()
+    rates = [repr(sweep.rate_for_load(x, sweep_run.parse_config_text(base), emu)) for x in (0.4, 0.8)]
+    cells = sweep_run.sweep_cells(["fs", "mfs"], rates, ["3"], ["1", "4"])
+    rows = [sweep_run.csv_header(True)]
+    got = np.load(os.path.join(out, "ttft.npz"))
+    for c in cells:
+        res = ref.run_config(base + f"policy = {c[0]}\nworkload.rate_rps = {c[1]}\n"
+                                    f"sim.seed = {c[2]}\nworkload.slo_multiplier = {c[3]}\n")
+        rows.append(sweep_run.csv_row(c, res.summary_json))
+        want = np.asarray(res.req_done) - np.asarray(res.req_arrival)
+        assert np.array_equal(got[sweep_run.cell_key(c) + "/ttft"], want, equal_nan=True)
+    assert rows[0].startswith("policy,rate_rps,seed,slo_multiplier,slo_attainment")
+    assert open(os.path.join(out, "sweep.csv")).read() == "".join(rows)
+    # the SLO multiplier changes attainment somewhere in the grid
+    assert len({r.split(",")[4] for r in rows[1:]}) > 1
