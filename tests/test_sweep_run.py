@@ -125,22 +125,24 @@ def test_sweep_on_device_matches_reference_simsweep(tmp_path):
     _check(out, conf)
 
 
-def test_slo_axis_and_loads_on_emulation(tmp_path):
+def _slo_axis_and_loads(tmp_path, lib):
     """SLO-multiplier and offered-load axes (configs[3]'s grid) with batch
     chunking: every row equals the reference run of the same cell"""
     from oracle import ref
     if not ref.available():
         pytest.skip("reference library (oracle/_ref) not built")
     from paper_2603_17456_b200 import sweep, sweep_run
-    from paper_2603_17456_b200.native import Native
-    emu = Native(os.path.join(ROOT, "build", "libmfsim_emu.so"))
+    from paper_2603_17456_b200.native import product
     conf = _conf(str(tmp_path))
     out = str(tmp_path / "o")
+    for k in ("RANK", "WORLD_SIZE", "LOCAL_RANK"):
+        os.environ.pop(k, None)
     sweep_run.main(["--config", conf, "--policies", "fs,mfs", "--loads", "0.4,0.8",
                     "--seeds", "3", "--slo-multipliers", "1,4", "--batch-cap", "3",
-                    "--no-reports", "--out", out], lib=emu, backend="gloo")
+                    "--no-reports", "--out", out], lib=lib, backend="gloo" if lib else None)
     base = open(conf).read()
-    rates = [repr(sweep.rate_for_load(x, sweep_run.parse_config_text(base), emu)) for x in (0.4, 0.8)]
+    rl = lib or product()
+    rates = [repr(sweep.rate_for_load(x, sweep_run.parse_config_text(base), rl)) for x in (0.4, 0.8)]
     cells = sweep_run.sweep_cells(["fs", "mfs"], rates, ["3"], ["1", "4"])
     rows = [sweep_run.csv_header(True)]
     got = np.load(os.path.join(out, "ttft.npz"))
@@ -154,3 +156,14 @@ def test_slo_axis_and_loads_on_emulation(tmp_path):
     assert open(os.path.join(out, "sweep.csv")).read() == "".join(rows)
     # the SLO multiplier changes attainment somewhere in the grid
     assert len({r.split(",")[4] for r in rows[1:]}) > 1
+
+
+def test_slo_axis_and_loads_on_emulation(tmp_path):
+    from paper_2603_17456_b200.native import Native
+    emu = Native(os.path.join(ROOT, "build", "libmfsim_emu.so"))
+    _slo_axis_and_loads(tmp_path, emu)
+
+
+@pytest.mark.gpu
+def test_slo_axis_and_loads_on_device(tmp_path):
+    _slo_axis_and_loads(tmp_path, None)
