@@ -55,8 +55,11 @@ __device__ __forceinline__ int sm_id() {
 
 // order[0, n): instance ids in claim groups (one per policy), estimated work
 // descending within a group; order[n + g] = offset of group g. A warp claims
-// from its SM's home group first -- SMs are mapped onto the groups in
-// proportion to their sizes -- then from the others.
+// from its SM's home group first, then from the others. SMs are mapped onto
+// the groups in proportion to their sizes for time-sliced launches (every
+// warp busy for the slice) and in proportion to their estimated work,
+// order[n + groups + 1 + g], for launches that run to completion (the
+// makespan is the most loaded SM's).
 template <bool kAalo>
 __global__ void __launch_bounds__(32)
     mfsim_engine_kernel(const Inst* __restrict__ insts, const int* __restrict__ order, int n,
@@ -76,8 +79,9 @@ __global__ void __launch_bounds__(32)
   const int* __restrict__ goff = order + n;
   int home = 0;
   {
+    const int* __restrict__ gmap = slice_ns > 0 ? goff : goff + groups + 1;
     const long long pos = (long long)sm_id() * n / nsm;
-    while (home + 1 < groups && goff[home + 1] <= pos) ++home;
+    while (home + 1 < groups && gmap[home + 1] <= pos) ++home;
   }
   for (;;) {
     int i = -1;

@@ -962,7 +962,7 @@ void Batch::pack() {
       st_dev_ = static_cast<char*>(be_.dev_alloc(st_bytes_ + 64));
       out_dev_ = static_cast<char*>(be_.dev_alloc(out_bytes_ + 64));
       desc_dev_ = static_cast<Inst*>(be_.dev_alloc(sizeof(Inst) * std::max(n, 1)));
-      order_dev_ = static_cast<int*>(be_.dev_alloc(sizeof(int) * (n + kMaxGroups + 1)));
+      order_dev_ = static_cast<int*>(be_.dev_alloc(sizeof(int) * (n + 2 * (kMaxGroups + 1))));
       phase_dev_ = static_cast<int*>(be_.dev_alloc(sizeof(int) * std::max(n, 1)));
     }
   }
@@ -991,6 +991,22 @@ void Batch::pack() {
   hint_.groups = static_cast<int>(off.size()) - 1;
   if (hint_.groups > kMaxGroups) throw InternalError("more claim groups than the kernel supports");
   order_.insert(order_.end(), off.begin(), off.end());
+  // SM -> home group map for launches that run to completion: SMs in
+  // proportion to each group's estimated WORK (its cost share, in [0, n)
+  // position units), so that the long (Karuna) instances spread over many
+  // SMs and the makespan is not one policy's SMs. Time-sliced launches keep
+  // the count-proportional map (every warp busy for the whole slice).
+  double total = 0.0;
+  for (int i = 0; i < n; ++i) total += cost[i];
+  std::vector<int> coff{0};
+  double acc = 0.0;
+  for (int g = 0; g + 1 < static_cast<int>(off.size()); ++g) {
+    for (int k = off[g]; k < off[g + 1]; ++k) acc += cost[order_[k]];
+    if (g + 2 < static_cast<int>(off.size()))
+      coff.push_back(std::max(coff.back(), std::min(n, static_cast<int>(total > 0 ? n * (acc / total) : off[g + 1]))));
+  }
+  coff.push_back(n);
+  order_.insert(order_.end(), coff.begin(), coff.end());
 }
 
 void Batch::upload_inputs() { be_.h2d(in_dev_, in_host_, in_bytes_); }

@@ -2,7 +2,10 @@
 the reference simulator (oracle/_ref) on a deterministic sample of cells.
 
   extract ttft.npz sample.npz   on the GPU box: keep the sampled cells' TTFTs
-  check sweep.csv sample.npz    here: run the reference on each sampled cell
+  precompute cache.npz          here, before the GPU run ends: the reference on
+                                the sampled cells of the grid (same rates)
+  check sweep.csv sample.npz [cache.npz]
+                                here: run the reference on each sampled cell
                                 (all host cores), compare the sweep.csv row and
                                 the per-request TTFTs bit for bit
 
@@ -52,15 +55,46 @@ def _ref_cell(key):
     return key, row, np.asarray(res.req_done) - np.asarray(res.req_arrival), res.events
 
 
-def check(csv_path, npz_path):
+def grid_keys():
+    from paper_2603_17456_b200 import sweep, sweep_run
+    from paper_2603_17456_b200.native import Native
+    emu = Native(os.path.join(ROOT, "build", "libmfsim_emu.so"))
+    rates = [repr(sweep.rate_for_load(x, sweep.FT128, emu)) for x in sweep.LOADS]
+    cells = sweep_run.sweep_cells(list(sweep.POLICIES), rates, [str(x) for x in range(1, 65)],
+                                  [str(x) for x in sweep.SLO_SCALES])
+    return [sweep_run.cell_key(c) for c in cells]
+
+
+def precompute(cache):
+    keys = sample_keys(grid_keys())
+    out = {}
+    with ProcessPoolExecutor(os.cpu_count()) as ex:
+        for key, row, ttft, ev in ex.map(_ref_cell, keys):
+            out[key + "/row"] = np.frombuffer(row.encode(), np.uint8)
+            out[key + "/ttft"] = ttft
+            out[key + "/events"] = np.array([ev])
+            print(key, ev, flush=True)
+    np.savez_compressed(cache, **out)
+
+
+def _cached(cache):
+    z = np.load(cache)
+    keys = [k[:-len("/row")] for k in z.files if k.endswith("/row")]
+    return {k: (k, z[k + "/row"].tobytes().decode(), z[k + "/ttft"], int(z[k + "/events"][0]))
+            for k in keys}
+
+
+def check(csv_path, npz_path, cache=None):
     _, body = rows(csv_path)
     by_key = {key_of_row(r): r for r in body}
     assert len(by_key) == 11200, len(by_key)
     z = np.load(npz_path)
     keys = [k.rsplit("/", 1)[0] for k in z.files]
     bad = 0
+    have = _cached(cache) if cache else {}
     with ProcessPoolExecutor(os.cpu_count()) as ex:
-        for key, row, ttft, ev in ex.map(_ref_cell, keys):
+        todo = [k for k in keys if k not in have]
+        for key, row, ttft, ev in [have[k] for k in keys if k in have] + list(ex.map(_ref_cell, todo)):
             ok_row = by_key[key] == row
             ok_ttft = np.array_equal(z[key + "/ttft"], ttft, equal_nan=True)
             bad += not (ok_row and ok_ttft)
@@ -74,5 +108,7 @@ def check(csv_path, npz_path):
 if __name__ == "__main__":
     if sys.argv[1] == "extract":
         extract(sys.argv[2], sys.argv[3])
+    elif sys.argv[1] == "precompute":
+        precompute(sys.argv[2])
     else:
-        sys.exit(1 if check(sys.argv[2], sys.argv[3]) else 0)
+        sys.exit(1 if check(sys.argv[2], sys.argv[3], *sys.argv[4:5]) else 0)
