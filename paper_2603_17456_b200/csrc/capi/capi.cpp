@@ -69,13 +69,25 @@ char* dup_string(const std::string& s) {
 }
 
 Report report_of(const InstanceInput& in, const InstanceOutput& o) {
-  std::vector<RowInput> rows(o.ttft.size());
-  for (size_t r = 0; r < rows.size(); ++r) {
-    const double arr = request_arrival(in, static_cast<int>(r));
-    const double dl = request_deadline(in, static_cast<int>(r));
-    rows[r] = RowInput{arr, dl, o.stall[r], o.ttft[r], o.pruned[r] != 0};
+  const long n = static_cast<long>(o.ttft.size());
+  std::vector<double> arr(n), dl(n);
+  for (long r = 0; r < n; ++r) {
+    arr[r] = request_arrival(in, static_cast<int>(r));
+    dl[r] = request_deadline(in, static_cast<int>(r));
   }
-  return reduce(rows, o.c_rel, o.c_done, o.c_stall, static_cast<long>(o.out[mfb::OUT_PRUNED]));
+  ReportColumns c;
+  c.arrival = arr.data();
+  c.deadline = dl.data();
+  c.done = o.ttft.data();
+  c.stall = o.stall.data();
+  c.pruned = o.pruned.data();
+  c.requests = n;
+  c.cof_release = o.c_rel.data();
+  c.cof_done = o.c_done.data();
+  c.cof_stall = o.c_stall.data();
+  c.coflows = static_cast<long>(o.c_done.size());
+  c.pruned_count = static_cast<long>(o.out[mfb::OUT_PRUNED]);
+  return summarize(c);
 }
 
 const InstanceOutput& checked(const mfsim_dev* d, int i) {
@@ -133,8 +145,8 @@ int mfsim_run(const mfsim_config* cfg, const char* out_dir, char** summary_json_
     const InstanceOutput& o = batch.output(0);
     raise_status(o.out[mfb::OUT_STATUS], o.out[mfb::OUT_CHECK]);
     Report rep = report_of(batch.input(0), o);
-    if (out_dir && *out_dir) write_files(rep, in.policy, in.seed, in.rate, out_dir);
-    if (summary_json_out) *summary_json_out = dup_string(json_text(rep, in.policy, in.seed, in.rate));
+    if (out_dir && *out_dir) write_report_files(rep, in.policy, in.seed, in.rate, out_dir);
+    if (summary_json_out) *summary_json_out = dup_string(summary_json_text(rep, in.policy, in.seed, in.rate));
   });
 }
 
@@ -368,7 +380,7 @@ int mfsim_dev_summary_json(const mfsim_dev* d, int i, char** out) {
     const InstanceOutput& o = checked(d, i);
     const InstanceInput& in = d->batch->input(i);
     raise_status(o.out[mfb::OUT_STATUS], o.out[mfb::OUT_CHECK]);
-    *out = dup_string(json_text(report_of(in, o), in.policy, in.seed, in.rate));
+    *out = dup_string(summary_json_text(report_of(in, o), in.policy, in.seed, in.rate));
   });
 }
 
@@ -378,7 +390,7 @@ int mfsim_dev_requests_csv(const mfsim_dev* d, int i, char** out) {
     const InstanceOutput& o = checked(d, i);
     const InstanceInput& in = d->batch->input(i);
     raise_status(o.out[mfb::OUT_STATUS], o.out[mfb::OUT_CHECK]);
-    *out = dup_string(csv_text(report_of(in, o)));
+    *out = dup_string(requests_csv_text(report_of(in, o)));
   });
 }
 
@@ -388,7 +400,7 @@ int mfsim_dev_write_report(const mfsim_dev* d, int i, const char* out_dir) {
     const InstanceOutput& o = checked(d, i);
     const InstanceInput& in = d->batch->input(i);
     raise_status(o.out[mfb::OUT_STATUS], o.out[mfb::OUT_CHECK]);
-    write_files(report_of(in, o), in.policy, in.seed, in.rate, out_dir);
+    write_report_files(report_of(in, o), in.policy, in.seed, in.rate, out_dir);
   });
 }
 

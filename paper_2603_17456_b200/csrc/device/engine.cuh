@@ -150,6 +150,7 @@ struct Sc {
   double horizon;
   unsigned long long seq;
   long long events, steps, streak, pushes, algo_bytes, classes, rounds;
+  long long stop_at;  // event count at which this launch suspends
   int n_flows, n_batches, n_coflows, n_active, n_ev;
   int rp_top, pp_top, cm_top;
   int next_arr;
@@ -205,7 +206,7 @@ template <class G, bool kAalo = true>
 struct Engine {
   G g;
   Inst& I;  // per-warp copy (shared memory on the device), arrays possibly re-pointed
-  const bool chip;
+  bool chip;
   Sc s;
 
   MF_FN explicit Engine(Inst& inst, bool on_chip = false) : I(inst), chip(on_chip) {}
@@ -1552,7 +1553,10 @@ MF_UNROLL
         for (int m = G::N / 2; m > 0; m >>= 1) cmin = smin(cmin, g.shfl_xor(cmin, m));
         const double athr = dadd(amin, dmul(amin, 0x1p-44));
         double inc = cmin;
-        if (amin <= cmin) {  // a link share may be the minimum: exact quotients near it
+        // a link share may be the minimum (allocator.cpp:88-93 takes min(q, cap gap)):
+        // exact quotients whenever the exact minimum can lie at or below cmin,
+        // i.e. within the approximation margin of amin
+        if (dsub(amin, dmul(amin, 0x1p-44)) <= cmin) {
           double q = MF_INF;
 MF_UNROLL
           for (int j = g.lane(); j < nt; j += G::N) {
@@ -1801,7 +1805,10 @@ MF_UNROLL
         }
         amin = g.min_nonneg(amin);  // smax(0, r) / cnt >= 0
         double inc = cmin;
-        if (amin <= cmin) {  // exact quotients only within the approximation margin
+        // exact quotients only within the approximation margin; the gate widens
+        // by the same margin so that an exact minimum just below cmin whose
+        // approximation rounded above it still wins (allocator.cpp:88-93)
+        if (dsub(amin, dmul(amin, 0x1p-18)) <= cmin) {
           const double athr = dadd(amin, dmul(amin, 0x1p-18));
           double q = MF_INF;
 MF_UNROLL
@@ -2986,9 +2993,22 @@ MF_UNROLL
   }
 
   // Runs the instance's event loop for at most `budget` events (<= 0: to the
-  // end) and, with deadline_ns, until the device clock passes it. A suspended instance keeps all state in HBM plus its scalar state in
-  // sc_blob and resumes exactly where it stopped. Returns true when finished.
+  // end) and, with deadline_ns, until the device clock passes it. A suspended
+  // instance keeps all state in HBM plus its scalar state in sc_blob and
+  // resumes exactly where it stopped. Returns true when finished. The loop is
+  // begin() / step() / end() so that a gang of warps can advance their
+  // instances one event at a time in lock step (engine_kernel.cu).
   MF_NOINLINE bool run(long long budget, unsigned long long deadline_ns = 0) {
+    if (!begin(budget)) return false;
+    int r;
+    do {
+      r = step(deadline_ns);
+    } while (r == 0);
+    return end(r == 1);
+  }
+
+  // resume or start; false when the instance finished in an earlier launch
+  MF_NOINLINE bool begin(long long budget) {
     static_assert(sizeof(Sc) <= kScBlob, "scalar state exceeds its blob");
     const int ph = *I.phase;
     if (ph == 2) return false;
@@ -3001,109 +3021,123 @@ MF_UNROLL
     } else {
       start();
     }
-    const long long stop_at = budget > 0 ? s.events + budget : 0x7fffffffffffffffLL;
-    bool finished = false;
-    while (!s.err) {
-      if (s.events >= stop_at) break;
-      if (deadline_ns && now_ns() >= deadline_ns) break;
-      MF_TIC(tn);
-      Ev e = next_event();
-      MF_TOC(OUT_CY_NEXT, tn);
-      if (e.src == 0 || e.t > s.horizon) {
-        finished = true;
+    s.stop_at = budget > 0 ? s.events + budget : 0x7fffffffffffffffLL;
+    return true;
+  }
+
+  // one iteration of Engine::run's loop (engine.cpp:598-655): 0 = go on,
+  // 1 = finished (or failed), 2 = suspend (event budget or deadline reached)
+  MF_NOINLINE int step(unsigned long long deadline_ns) {
+    const int r = step_event(deadline_ns);
+    if (r == 0) settle();
+    return s.err ? 1 : r;
+  }
+  // the rate recomputation that closes an event (engine.cpp:651-654)
+  MF_NOINLINE void settle() {
+    if (s.dirty && !s.err) {
+      recompute_rates();
+      s.dirty = 0;
+    }
+  }
+  // the event itself: pop, advance, dispatch; leaves s.dirty for settle()
+  MF_NOINLINE int step_event(unsigned long long deadline_ns) {
+    if (s.err) return 1;
+    if (s.events >= s.stop_at) return 2;
+    if (deadline_ns && now_ns() >= deadline_ns) return 2;
+    MF_TIC(tn);
+    Ev e = next_event();
+    MF_TOC(OUT_CY_NEXT, tn);
+    if (e.src == 0 || e.t > s.horizon) return 1;
+    int kind, a, b;
+    if (e.src == 1) {
+      kind = EV_ARRIVAL;
+      a = e.idx;
+      b = -1;
+      ++s.next_arr;
+    } else if (e.src == 2) {
+      kind = I.e_kind[e.idx];
+      a = I.e_a[e.idx];
+      b = I.e_b[e.idx];
+      pool_remove(e.idx);
+    } else {
+      kind = EV_FLOW;
+      a = I.a_fid[e.idx];
+      b = -1;
+    }
+    MF_TIC(ta);
+    advance_to(e.t);
+    MF_TOC(OUT_CY_ADVANCE, ta);
+    if (s.err) return 1;
+#if defined(MF_TRACE) && !defined(__CUDACC__)
+    fprintf(stderr, "ev %lld t=%.17g kind=%d a=%d b=%d nact=%d nev=%d\n", s.events, e.t, kind, a, b,
+            s.n_active, s.n_ev);
+#endif
+    ++s.events;
+    if (e.t == s.prev_t) {
+      if (++s.streak > I.p.livelock) {
+        fail(ERR_SIM, CHK_LIVELOCK);
+        return 1;
+      }
+    } else {
+      s.streak = 0;
+      s.prev_t = e.t;
+    }
+    MF_TIC(th);
+    switch (kind) {
+      case EV_FLOW: {
+        MF_TIC(h0);
+        finish_flow(a);
+        MF_TOC(OUT_CY_SUB + 6, h0);
         break;
       }
-      int kind, a, b;
-      if (e.src == 1) {
-        kind = EV_ARRIVAL;
-        a = e.idx;
-        b = -1;
-        ++s.next_arr;
-      } else if (e.src == 2) {
-        kind = I.e_kind[e.idx];
-        a = I.e_a[e.idx];
-        b = I.e_b[e.idx];
-        pool_remove(e.idx);
-      } else {
-        kind = EV_FLOW;
-        a = I.a_fid[e.idx];
-        b = -1;
+      case EV_COMPUTE: {
+        MF_TIC(h1);
+        handle_compute_complete(a, b);
+        MF_TOC(OUT_CY_SUB + 8, h1);
+        break;
       }
-      MF_TIC(ta);
-      advance_to(e.t);
-      MF_TOC(OUT_CY_ADVANCE, ta);
-      if (s.err) break;
-#if defined(MF_TRACE) && !defined(__CUDACC__)
-      fprintf(stderr, "ev %lld t=%.17g kind=%d a=%d b=%d nact=%d nev=%d\n", s.events, e.t, kind, a, b,
-              s.n_active, s.n_ev);
-#endif
-      ++s.events;
-      if (e.t == s.prev_t) {
-        if (++s.streak > I.p.livelock) {
-          fail(ERR_SIM, CHK_LIVELOCK);
-          break;
-        }
-      } else {
-        s.streak = 0;
-        s.prev_t = e.t;
+      case EV_DEPART: {
+        MF_TIC(h2);
+        handle_batch_depart(a);
+        MF_TOC(OUT_CY_SUB + 9, h2);
+        break;
       }
-      MF_TIC(th);
-      switch (kind) {
-        case EV_FLOW: {
-          MF_TIC(h0);
-          finish_flow(a);
-          MF_TOC(OUT_CY_SUB + 6, h0);
-          break;
-        }
-        case EV_COMPUTE: {
-          MF_TIC(h1);
-          handle_compute_complete(a, b);
-          MF_TOC(OUT_CY_SUB + 8, h1);
-          break;
-        }
-        case EV_DEPART: {
-          MF_TIC(h2);
-          handle_batch_depart(a);
-          MF_TOC(OUT_CY_SUB + 9, h2);
-          break;
-        }
-        case EV_ARRIVAL: {
-          const int u = I.r_unit[a];
-          put(&I.q_tail[u], I.q_tail[u] + 1);
-          push(s.now, EV_ADMIT, u, -1);
-          break;
-        }
-        case EV_ADMIT: {
-          MF_TIC(h3);
-          if (I.p.workload_mode)
-            handle_admit_try(a);
-          else
-            activate_manual_batch(a);
-          MF_TOC(OUT_CY_SUB + 10, h3);
-          break;
-        }
-        case EV_RELEASE:
-          if (I.f_state[a] == FL_PENDING) release_flow(a);
-          break;
-        case EV_TICK: {
-          if (p2d_left(a)) {
-            if (promote_batch(a, true)) s.dirty = 1;
-            push(dadd(s.now, I.p.tick), EV_TICK, a, -1);
-          }
-          break;
-        }
-        default:
-          break;
+      case EV_ARRIVAL: {
+        const int u = I.r_unit[a];
+        put(&I.q_tail[u], I.q_tail[u] + 1);
+        push(s.now, EV_ADMIT, u, -1);
+        break;
       }
-      MF_TOC(OUT_CY_HANDLER, th);
-      if (s.err) break;
-      if (s.dirty) {
-        recompute_rates();
-        s.dirty = 0;
+      case EV_ADMIT: {
+        MF_TIC(h3);
+        if (I.p.workload_mode)
+          handle_admit_try(a);
+        else
+          activate_manual_batch(a);
+        MF_TOC(OUT_CY_SUB + 10, h3);
+        break;
       }
+      case EV_RELEASE:
+        if (I.f_state[a] == FL_PENDING) release_flow(a);
+        break;
+      case EV_TICK: {
+        if (p2d_left(a)) {
+          if (promote_batch(a, true)) s.dirty = 1;
+          push(dadd(s.now, I.p.tick), EV_TICK, a, -1);
+        }
+        break;
+      }
+      default:
+        break;
     }
+    MF_TOC(OUT_CY_HANDLER, th);
+    return s.err ? 1 : 0;
+  }
+
+  // suspend (scalar state and pool to HBM) or finalize and publish the outputs
+  MF_NOINLINE bool end(bool finished) {
     if (s.err) finished = true;
-    if (!finished) {  // suspend: scalar state and pool to HBM
+    if (!finished) {
       g.sync();
       if (g.leader()) {
         const unsigned int* src = reinterpret_cast<const unsigned int*>(&s);

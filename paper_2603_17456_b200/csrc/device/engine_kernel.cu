@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <stdexcept>
 #include <string>
 
@@ -53,6 +54,89 @@ __device__ __forceinline__ int sm_id() {
   return (int)r;
 }
 
+// Copies instance `src`'s descriptor into this warp's shared-memory region
+// `base` and stages the event pool and the per-slot filling state there when
+// the instance's capacities fit the plan. Returns whether the slot state is on
+// chip (the filling rounds are specialised on it).
+__device__ __noinline__ bool stage_instance(const Inst* __restrict__ src, unsigned char* base,
+                                            const SmemPlan& plan) {
+  const int lane = threadIdx.x & 31;
+  Inst* d = reinterpret_cast<Inst*>(base);
+  {  // descriptor copy (8-byte words across the warp)
+    const unsigned long long* s8 = reinterpret_cast<const unsigned long long*>(src);
+    unsigned long long* d8 = reinterpret_cast<unsigned long long*>(d);
+    for (int w = lane; w < (int)(sizeof(Inst) / 8); w += 32) d8[w] = s8[w];
+  }
+  __syncwarp();
+  bool slots_on_chip = false;
+  if (lane == 0) {
+    unsigned char* q = base + align16(sizeof(Inst));
+    auto take = [&](int bytes) {
+      unsigned char* r = q;
+      q += align16(bytes);
+      return r;
+    };
+    if (d->E_cap <= plan.ES) {
+      double* et = reinterpret_cast<double*>(take(plan.ES * 8));
+      unsigned long long* es = reinterpret_cast<unsigned long long*>(take(plan.ES * 8));
+      int* ek = reinterpret_cast<int*>(take(plan.ES * 4));
+      int* ea = reinterpret_cast<int*>(take(plan.ES * 4));
+      int* eb = reinterpret_cast<int*>(take(plan.ES * 4));
+      d->e_t_home = d->e_t;  // the engine moves entries between chip and home
+      d->e_seq_home = d->e_seq;
+      d->e_kind_home = d->e_kind;
+      d->e_a_home = d->e_a;
+      d->e_b_home = d->e_b;
+      d->e_t = et;
+      d->e_seq = es;
+      d->e_kind = ek;
+      d->e_a = ea;
+      d->e_b = eb;
+    } else {
+      q += 2 * align16(plan.ES * 8) + 3 * align16(plan.ES * 4);
+    }
+    if (plan.TS > 0 && d->TS_cap > 0 && d->A_cap <= 32 * kFrzWords) {
+      // per-step slot state on chip; the slot bookkeeping stays in HBM
+      // (its capacity bound must not change across suspend / resume)
+      d->sl_res = reinterpret_cast<double*>(take(plan.TS * 8));
+      d->sl_cnt = reinterpret_cast<int*>(take(plan.TS * 4));
+      d->sl_mb = reinterpret_cast<int*>(take(plan.TS * 4));
+      d->sl_end = reinterpret_cast<int*>(take(plan.TS * 4));
+      d->sl_tl = reinterpret_cast<unsigned short*>(take(plan.TS * 2));
+      d->sl_sat = reinterpret_cast<unsigned short*>(take(plan.TS * 2));
+      d->c_frz = reinterpret_cast<unsigned*>(take(kFrzWords * 4));
+      slots_on_chip = true;
+    }
+  }
+  slots_on_chip = __shfl_sync(0xffffffffu, slots_on_chip, 0);
+  __syncwarp();
+  return slots_on_chip;
+}
+
+// The SM's home claim group (see the kernels below).
+__device__ __forceinline__ int home_group(const int* __restrict__ goff, int n, int groups, int nsm,
+                                          long long slice_ns) {
+  int home = 0;
+  const int* __restrict__ gmap = slice_ns > 0 ? goff : goff + groups + 1;
+  const long long pos = (long long)sm_id() * n / nsm;
+  while (home + 1 < groups && gmap[home + 1] <= pos) ++home;
+  return home;
+}
+
+// next instance for this warp (-1: none left), home group first
+__device__ __forceinline__ int claim(const int* __restrict__ order, const int* __restrict__ goff,
+                                     int groups, int home, int* __restrict__ next) {
+  int i = -1;
+  if ((threadIdx.x & 31) == 0) {
+    for (int k = 0; k < groups && i < 0; ++k) {
+      const int gi = (home + k) % groups;
+      const int c = atomicAdd(&next[gi], 1);
+      if (goff[gi] + c < goff[gi + 1]) i = order[goff[gi] + c];
+    }
+  }
+  return __shfl_sync(0xffffffffu, i, 0);
+}
+
 // order[0, n): instance ids in claim groups (one per policy), estimated work
 // descending within a group; order[n + g] = offset of group g. A warp claims
 // from its SM's home group first, then from the others. SMs are mapped onto
@@ -77,75 +161,77 @@ __global__ void __launch_bounds__(32)
     deadline = t0 + (unsigned long long)slice_ns;
   }
   const int* __restrict__ goff = order + n;
-  int home = 0;
-  {
-    const int* __restrict__ gmap = slice_ns > 0 ? goff : goff + groups + 1;
-    const long long pos = (long long)sm_id() * n / nsm;
-    while (home + 1 < groups && gmap[home + 1] <= pos) ++home;
-  }
+  const int home = home_group(goff, n, groups, nsm, slice_ns);
   for (;;) {
-    int i = -1;
-    if (lane == 0) {
-      for (int k = 0; k < groups && i < 0; ++k) {
-        const int gi = (home + k) % groups;
-        const int c = atomicAdd(&next[gi], 1);
-        if (goff[gi] + c < goff[gi + 1]) i = order[goff[gi] + c];
-      }
-    }
-    i = __shfl_sync(0xffffffffu, i, 0);
+    const int i = claim(order, goff, groups, home, next);
     if (i < 0) return;
-    {  // descriptor copy (8-byte words across the warp)
-      const unsigned long long* src = reinterpret_cast<const unsigned long long*>(insts + i);
-      unsigned long long* dst = reinterpret_cast<unsigned long long*>(d);
-      for (int w = lane; w < (int)(sizeof(Inst) / 8); w += 32) dst[w] = src[w];
-    }
-    __syncwarp();
-    bool slots_on_chip = false;
-    if (lane == 0) {
-      unsigned char* q = smem + align16(sizeof(Inst));
-      auto take = [&](int bytes) {
-        unsigned char* r = q;
-        q += align16(bytes);
-        return r;
-      };
-      if (d->E_cap <= plan.ES) {
-        double* et = reinterpret_cast<double*>(take(plan.ES * 8));
-        unsigned long long* es = reinterpret_cast<unsigned long long*>(take(plan.ES * 8));
-        int* ek = reinterpret_cast<int*>(take(plan.ES * 4));
-        int* ea = reinterpret_cast<int*>(take(plan.ES * 4));
-        int* eb = reinterpret_cast<int*>(take(plan.ES * 4));
-        d->e_t_home = d->e_t;  // the engine moves entries between chip and home
-        d->e_seq_home = d->e_seq;
-        d->e_kind_home = d->e_kind;
-        d->e_a_home = d->e_a;
-        d->e_b_home = d->e_b;
-        d->e_t = et;
-        d->e_seq = es;
-        d->e_kind = ek;
-        d->e_a = ea;
-        d->e_b = eb;
-      } else {
-        q += 2 * align16(plan.ES * 8) + 3 * align16(plan.ES * 4);
-      }
-      if (plan.TS > 0 && d->TS_cap > 0 && d->A_cap <= 32 * kFrzWords) {
-        // per-step slot state on chip; the slot bookkeeping stays in HBM
-        // (its capacity bound must not change across suspend / resume)
-        d->sl_res = reinterpret_cast<double*>(take(plan.TS * 8));
-        d->sl_cnt = reinterpret_cast<int*>(take(plan.TS * 4));
-        d->sl_mb = reinterpret_cast<int*>(take(plan.TS * 4));
-        d->sl_end = reinterpret_cast<int*>(take(plan.TS * 4));
-        d->sl_tl = reinterpret_cast<unsigned short*>(take(plan.TS * 2));
-        d->sl_sat = reinterpret_cast<unsigned short*>(take(plan.TS * 2));
-        d->c_frz = reinterpret_cast<unsigned*>(take(kFrzWords * 4));
-        slots_on_chip = true;
-      }
-    }
-    slots_on_chip = __shfl_sync(0xffffffffu, slots_on_chip, 0);
-    __syncwarp();
+    const bool slots_on_chip = stage_instance(insts + i, smem, plan);
     Engine<WarpLanes, kAalo> eng(*d, slots_on_chip);
     const bool done = eng.run(budget, deadline);
     if (done && lane == 0) atomicSub(remaining, 1);
     __syncwarp();
+  }
+}
+
+// Gang variant: a block of W warps, each owning its own instance (and its own
+// slice of shared memory), advances all W instances ONE EVENT at a time in
+// lock step (one block barrier per event). The engine is instruction-fetch
+// bound (ncu: 50-68 % of warp stalls "no instruction", ~40k SASS instructions,
+// warps of one SM in different phases); in lock step the W warps of a block
+// run through the same code at about the same time.
+template <bool kAalo>
+__global__ void __launch_bounds__(1024, 1)
+    mfsim_gang_kernel(const Inst* __restrict__ insts, const int* __restrict__ order, int n,
+                      int groups, int nsm, int* __restrict__ next, SmemPlan plan,
+                      long long budget, long long slice_ns, int* __restrict__ remaining,
+                      long long quantum, int split) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ unsigned long long t0;
+  const int lane = threadIdx.x & 31;
+  unsigned char* mine = smem + (threadIdx.x >> 5) * plan.bytes;
+  Inst* d = reinterpret_cast<Inst*>(mine);
+  unsigned long long deadline = 0;
+  if (slice_ns > 0) {
+    if (threadIdx.x == 0) t0 = now_ns();
+    __syncthreads();
+    deadline = t0 + (unsigned long long)slice_ns;
+  }
+  const int* __restrict__ goff = order + n;
+  const int home = home_group(goff, n, groups, nsm, slice_ns);
+  Engine<WarpLanes, kAalo> eng(*d, false);
+  int state = 0;  // 0: claim next, 1: running an instance, 2: no work left
+  for (;;) {
+    if (state == 0) {
+      const int i = claim(order, goff, groups, home, next);
+      if (i < 0) {
+        state = 2;
+      } else {
+        eng.chip = stage_instance(insts + i, mine, plan);
+        if (eng.begin(budget)) state = 1;
+      }
+    }
+    int r = 0;
+    if (state == 1) {
+      if (split) {  // the event, then (after a barrier) its rate recomputation
+        r = eng.step_event(deadline);
+      } else {
+        const long long c0 = clock64();
+        do {
+          r = eng.step(deadline);
+        } while (r == 0 && clock64() - c0 < quantum);
+      }
+    }
+    if (split) {
+      __syncthreads();
+      if (state == 1 && r == 0) eng.settle();
+    }
+    if (state == 1 && r != 0) {
+      const bool done = eng.end(r == 1);
+      if (done && lane == 0) atomicSub(remaining, 1);
+      __syncwarp();
+      state = 0;
+    }
+    if (!__syncthreads_or(state != 2)) break;
   }
 }
 
@@ -171,8 +257,16 @@ class CudaBackend final : public Backend {
     ck(cudaMallocHost(&remain_host_, sizeof(int)), "cudaMallocHost");
     ck(cudaDeviceGetAttribute(&sms_, cudaDevAttrMultiProcessorCount, device), "attr");
     for (auto k : {mfb::mfsim_engine_kernel<false>, mfb::mfsim_engine_kernel<true>})
-      ck(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024),
+      ck(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024),
          "smem attr");
+    for (auto k : {mfb::mfsim_gang_kernel<false>, mfb::mfsim_gang_kernel<true>})
+      ck(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024),
+         "smem attr");
+    if (const char* g = getenv("MFSIM_GANG")) gang_ = atoi(g);
+    if (gang_ < 1) gang_ = 1;
+    if (gang_ > 32) gang_ = 32;
+    if (const char* q = getenv("MFSIM_GANG_Q")) quantum_ = atoll(q);
+    if (const char* q = getenv("MFSIM_GANG_SPLIT")) split_ = atoi(q);
     // deep per-warp call chains (noinline handlers) need more than the default
     ck(cudaDeviceSetLimit(cudaLimitStackSize, 4096), "stack limit");
   }
@@ -205,6 +299,10 @@ class CudaBackend final : public Backend {
   void launch(const mfb::Inst* d, const int* order, int n, const LaunchHint& hint,
               long long budget, long long slice_ns) override {
     const mfb::SmemPlan plan = mfb::make_plan(hint.nlinks);
+    if (gang_ > 1) {
+      launch_gang(d, order, n, hint, budget, slice_ns, plan);
+      return;
+    }
     int per_sm = 0;
     // the lean kernel unless the batch holds Aalo instances (extension code compiled out)
     auto kern = hint.aalo ? mfb::mfsim_engine_kernel<true> : mfb::mfsim_engine_kernel<false>;
@@ -218,6 +316,27 @@ class CudaBackend final : public Backend {
     ck(cudaEventRecord(e0_, stream_), "event");
     kern<<<grid, 32, plan.bytes, stream_>>>(
         d, order, n, hint.groups, sms_, counter_ + 1, plan, budget, slice_ns, counter_);
+    ck(cudaGetLastError(), "launch");
+    ck(cudaEventRecord(e1_, stream_), "event");
+    ++launches_;
+    timed_ = true;
+    last_grid_ = grid;
+  }
+  void launch_gang(const mfb::Inst* d, const int* order, int n, const LaunchHint& hint,
+                   long long budget, long long slice_ns, const mfb::SmemPlan& plan) {
+    auto kern = hint.aalo ? mfb::mfsim_gang_kernel<true> : mfb::mfsim_gang_kernel<false>;
+    const int threads = 32 * gang_;
+    const int bytes = plan.bytes * gang_;
+    int per_sm = 0;
+    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, bytes), "occupancy");
+    if (per_sm < 1) throw DeviceError("gang block does not fit an SM");
+    int grid = sms_ * per_sm;
+    const int need = (n + gang_ - 1) / gang_;
+    if (need < grid) grid = need > 0 ? need : 1;
+    ck(cudaMemsetAsync(counter_ + 1, 0, sizeof(int) * kMaxGroups, stream_), "memset");
+    ck(cudaEventRecord(e0_, stream_), "event");
+    kern<<<grid, threads, bytes, stream_>>>(d, order, n, hint.groups, sms_, counter_ + 1, plan,
+                                             budget, slice_ns, counter_, quantum_, split_);
     ck(cudaGetLastError(), "launch");
     ck(cudaEventRecord(e1_, stream_), "event");
     ++launches_;
@@ -257,6 +376,9 @@ class CudaBackend final : public Backend {
   int* counter_ = nullptr;
   int* remain_host_ = nullptr;
   int sms_ = 148;
+  int gang_ = 1;  // warps per block in lock step (MFSIM_GANG, A/B)
+  long long quantum_ = 0;  // SM cycles of events per warp between barriers (MFSIM_GANG_Q)
+  int split_ = 0;  // barrier between an event and its rate recomputation (MFSIM_GANG_SPLIT)
   int last_grid_ = 0;
   int launches_ = 0;
   bool timed_ = false;

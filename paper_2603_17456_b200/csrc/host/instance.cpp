@@ -398,15 +398,28 @@ void derive_deadlines(Backend& be, const std::vector<InstanceInput*>& insts) {
     put(fsp.alpha), put(fsp.beta), put(fsp.kv), put(fsp.coll), put(fsp.units), put(fsp.hpu);
     put(fsp.decode_hosts), put(fsp.prune_enable), put(fsp.drop_frac), put(fsp.workload_mode);
     probe_of[i].resize(in.reqs.size());
+    // Within an instance the reference caches on the reuse fraction rounded to
+    // 1e-9 (workload.cpp:203-205): a request reuses the isolated TTFT of the
+    // FIRST request of its (tokens, llround(frac * 1e9), unit, source) bucket.
+    std::map<std::tuple<long, long, int, int>, int> bucket;
     for (size_t r = 0; r < in.reqs.size(); ++r) {
       const HostRequest& q = in.reqs[r];
-      long bits;  // the exact reuse fraction
+      const auto bk = std::make_tuple(static_cast<long>(q.tokens),
+                                      static_cast<long>(std::llround(q.reuse * 1e9)), q.unit, q.source);
+      if (auto b = bucket.find(bk); b != bucket.end()) {
+        probe_of[i][r] = b->second;
+        continue;
+      }
+      // the bucket's first request: its probe is shared across instances by
+      // the exact reuse bits (the run depends on the exact fraction)
+      long bits;
       std::memcpy(&bits, &q.reuse, sizeof(bits));
       auto key = std::make_tuple(static_cast<const void*>(in.topo.get()), pkey, q.tokens, bits, q.unit,
                                  q.source);
       auto it = cache.find(key);
       if (it != cache.end()) {
         probe_of[i][r] = it->second;
+        bucket.emplace(bk, it->second);
         continue;
       }
       InstanceInput p;
@@ -420,6 +433,7 @@ void derive_deadlines(Backend& be, const std::vector<InstanceInput*>& insts) {
       const int id = static_cast<int>(probes.size());
       probes.push_back(std::move(p));
       cache.emplace(key, id);
+      bucket.emplace(bk, id);
       probe_of[i][r] = id;
     }
   }
@@ -563,7 +577,11 @@ void carve_instance(Carver& c, const InstanceInput& in, Inst& d, const Inst& top
     for (auto& cf : m->coflows) CM += static_cast<long>(cf.members.size());
     E = B * 3 + F + 64 + in.e_boost;
   }
-  A = in.a_cap > 0 ? in.a_cap : std::min<long>(std::max<long>(F, 1), kDefaultActive);
+  // first-attempt active-set bound: the on-chip plan's 1024, or MFSIM_ACTIVE_CAP
+  // for runs known to be large (an overflow re-runs the batch from the start)
+  long a_first = kDefaultActive;
+  if (const char* e = std::getenv("MFSIM_ACTIVE_CAP")) a_first = std::max(1L, std::atol(e));
+  A = in.a_cap > 0 ? in.a_cap : std::min<long>(std::max<long>(F, 1), a_first);
 
   A = std::max<long>(A, 1);
   const long X = A * d.rmax;
@@ -1109,7 +1127,8 @@ void Batch::run(int detail) {
         in.e_boost = std::max(in.e_boost * 2, 1024);
         again = true;
       } else if (chk == CHK_CAP_ACTIVE || chk == CHK_CAP_SCRATCH) {
-        const long long grown = std::max<long long>(2LL * desc_[i].A_cap, 64);
+        // x4: an overflow means a large instance, and every retry re-runs it
+        const long long grown = std::max<long long>(4LL * desc_[i].A_cap, 64);
         in.a_cap = static_cast<int>(std::min<long long>(grown, std::max(desc_[i].F_cap, 1)));
         again = true;
       }

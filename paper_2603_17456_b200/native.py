@@ -321,9 +321,13 @@ def route(cfg, src: int, dst: int, lib: Native | None = None):
     n = lib or product()
     if not isinstance(cfg, Config):
         cfg = Config(cfg, n)
-    links, caps, cnt = np.zeros(64, np.int32), np.zeros(64), C.c_int(0)
-    n.check(n.lib.mfsim_route(cfg.h, src, dst, _ptr(links), _ptr(caps), 64, C.byref(cnt)))
-    return links[:cnt.value].tolist(), caps[:cnt.value].tolist()
+    size = 64
+    while True:
+        links, caps, cnt = np.zeros(size, np.int32), np.zeros(size), C.c_int(0)
+        n.check(n.lib.mfsim_route(cfg.h, src, dst, _ptr(links), _ptr(caps), size, C.byref(cnt)))
+        if cnt.value <= size:
+            return links[:cnt.value].tolist(), caps[:cnt.value].tolist()
+        size = cnt.value  # a longer route than the buffers: call again with room for it
 
 
 def link_count(cfg, lib: Native | None = None) -> int:

@@ -75,6 +75,19 @@ def _zipf(self_u: int, units: int, skew: float):
     return {v: x / s for v, x in w.items()}
 
 
+# the simulator's defaults for the keys the load model reads (config.cpp,
+# CostModel / Layout / WorkloadSpec::from; decode_hosts defaults to the unit count)
+LIB_DEFAULTS = {
+    "cluster.prefill_units": 1,
+    "cluster.hosts_per_unit": 2,
+    "model.layers": 4,
+    "model.kv_bytes_per_token_layer": 1000.0,
+    "model.coll_bytes_per_token_layer": 250.0,
+    "workload.prompt_mean_tokens": 2000.0,
+    "workload.reuse_fraction_mean": 0.5,
+    "workload.reuse_skew": 1.0,
+}
+
 _util_cache: dict = {}
 
 
@@ -86,15 +99,17 @@ def busiest_link_bytes(base: dict, lib=None) -> float:
     if key in _util_cache:
         return _util_cache[key]
     cfg = Config(text(base), lib)
-    U = int(base["cluster.prefill_units"])
-    H = int(base["cluster.hosts_per_unit"])
-    D = int(base["cluster.decode_hosts"])
-    L = float(base["model.layers"])
-    T = float(base["workload.prompt_mean_tokens"])
-    kv = float(base["model.kv_bytes_per_token_layer"])
-    coll = float(base["model.coll_bytes_per_token_layer"])
-    r = float(base["workload.reuse_fraction_mean"])
-    skew = float(base["workload.reuse_skew"])
+    # keys the file leaves out take the simulator's defaults (config.cpp)
+    eff = dict(LIB_DEFAULTS, **base)
+    U = int(eff["cluster.prefill_units"])
+    H = int(eff["cluster.hosts_per_unit"])
+    D = int(eff.get("cluster.decode_hosts", U))
+    L = float(eff["model.layers"])
+    T = float(eff["workload.prompt_mean_tokens"])
+    kv = float(eff["model.kv_bytes_per_token_layer"])
+    coll = float(eff["model.coll_bytes_per_token_layer"])
+    r = float(eff["workload.reuse_fraction_mean"])
+    skew = float(eff["workload.reuse_skew"])
     load = [0.0] * link_count(cfg, lib)
     cap = [1.0] * len(load)
 

@@ -51,6 +51,43 @@ def test_arrivals_and_deadlines_match_reference(emu):
         assert np.array_equal(r.req_deadline.view(np.int64), dl.view(np.int64))
 
 
+def test_deadline_cache_buckets_reuse_fraction(emu, tmp_path):
+    """derive_slos keys its cache on llround(reuse_fraction * 1e9) (workload.cpp:203-205):
+    a request whose fraction differs from an earlier one only below 1e-9 reuses that
+    request's isolated TTFT, so its deadline is NOT its own probe's"""
+    from oracle import ref
+    if not ref.available():
+        pytest.skip("oracle/_ref not built")
+    units = 8
+    rows = ["arrival_s,prompt_tokens,reuse_fraction,source_unit"]
+    fr = [0.3, 0.3 + 3e-12, 0.3 - 4e-11, 0.5, 0.5 + 2e-10, 0.3 + 6e-10]
+    for k, f in enumerate(fr):  # request k * units lands on unit 0 (round robin)
+        for u in range(units):
+            rows.append(f"{(k * units + u) * 0.05:.9f},1500,{f if u == 0 else 0.25!r},{(u + 1) % units}")
+    trace = tmp_path / "near.csv"
+    trace.write_text("\n".join(rows) + "\n")
+    text = open("tests/configs/cluster8.conf").read() + f"workload.trace = {trace}\npolicy = mfs\n"
+    arr, dl = ref.derive_deadlines(text)
+    b = DeviceBatch(0, emu)
+    b.add_config(text)
+    b.add_config(text + "policy = fs\n")  # cross-instance probe sharing
+    b.prepare()
+    b.run(0)
+    for i in range(2):
+        r = b.result(i, 0)
+        assert np.array_equal(r.req_arrival.view(np.int64), arr.view(np.int64))
+        assert np.array_equal(r.req_deadline.view(np.int64), dl.view(np.int64))
+
+
+def test_load_model_uses_library_defaults(emu):
+    """a base config that omits keys gets the simulator's defaults (config.cpp), not a KeyError"""
+    base = {k: v for k, v in sweep.FT128.items()
+            if k not in ("model.coll_bytes_per_token_layer", "model.layers", "workload.reuse_skew")}
+    full = dict(base, **{"model.coll_bytes_per_token_layer": 250.0, "model.layers": 4,
+                         "workload.reuse_skew": 1.0})
+    assert sweep.busiest_link_bytes(base, lib=emu) == sweep.busiest_link_bytes(full, lib=emu)
+
+
 def test_sweep_grid():
     cells = sweep.sweep_cells()
     assert len(cells) == 7 * 5 * 64 * 5 == 11200
