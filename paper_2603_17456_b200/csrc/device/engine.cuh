@@ -1532,13 +1532,28 @@ MF_UNROLL
         // is within 2 ulp of the correctly rounded res / cnt, so every link
         // whose exact quotient can be the minimum lies within that margin of
         // the approximate minimum; only those are divided exactly.
-        double amin = MF_INF;
+        // lane-best share with its (residual, count) and the runner-up of a
+        // different pair, as in allocate_slots
+        double lmin = MF_INF, b2 = MF_INF, r1 = 0.0;
+        int c1 = 1;
 MF_UNROLL
         for (int j = g.lane(); j < nt; j += G::N) {
           const int l = tl[j];
           const int cn = cnt[l];
           const double r = res[l];
-          if (cn > 0) amin = smin(amin, dmul(smax(0.0, r), recip(cn)));
+          if (cn > 0) {
+            const double rr = smax(0.0, r);
+            const double a = dmul(rr, recip(cn));
+            const bool other = !(rr == r1 && cn == c1);
+            if (a < lmin) {
+              if (other) b2 = lmin;
+              lmin = a;
+              r1 = rr;
+              c1 = cn;
+            } else if (other) {
+              b2 = smin(b2, a);
+            }
+          }
         }
         double cmin = MF_INF;
         if (has_caps) {
@@ -1549,7 +1564,7 @@ MF_UNROLL
             if (cp < MF_INF) cmin = smin(cmin, dsub(smax(0.0, cp), rate[p]));
           }
         }
-        amin = g.min_nonneg(amin);
+        const double amin = g.min_nonneg(lmin);
         for (int m = G::N / 2; m > 0; m >>= 1) cmin = smin(cmin, g.shfl_xor(cmin, m));
         const double athr = dadd(amin, dmul(amin, 0x1p-44));
         double inc = cmin;
@@ -1558,12 +1573,16 @@ MF_UNROLL
         // i.e. within the approximation margin of amin
         if (dsub(amin, dmul(amin, 0x1p-44)) <= cmin) {
           double q = MF_INF;
+          if (g.any(b2 <= athr)) {
 MF_UNROLL
-          for (int j = g.lane(); j < nt; j += G::N) {
-            const int l = tl[j];
-            const int cn = cnt[l];
-            const double r = smax(0.0, res[l]);
-            if (cn > 0 && dmul(r, recip(cn)) <= athr) q = smin(q, ddiv(r, (double)cn));
+            for (int j = g.lane(); j < nt; j += G::N) {
+              const int l = tl[j];
+              const int cn = cnt[l];
+              const double r = smax(0.0, res[l]);
+              if (cn > 0 && dmul(r, recip(cn)) <= athr) q = smin(q, ddiv(r, (double)cn));
+            }
+          } else if (lmin <= athr) {
+            q = ddiv(r1, (double)c1);
           }
           inc = smin(inc, g.min_nonneg(q));  // as in allocate_slots
         }
@@ -1795,28 +1814,51 @@ MF_UNROLL
         ++rounds;
         MF_TIC(q2);
         const double cmin = ncap > 0 ? dsub(cmn, R) : MF_INF;
-        double amin = MF_INF;
+        // Approximate shares max(0,res)/cnt through a single-precision
+        // reciprocal (relative error < 2^-23). Each lane keeps its best share
+        // with its (residual, count) and the best share of a DIFFERENT
+        // (residual, count) pair: when no lane's runner-up lies within the
+        // margin of the warp minimum, the exact minimum is among the lanes'
+        // best pairs and one division per lane settles it; otherwise a second
+        // pass divides every share within the margin.
+        double lmin = MF_INF, b2 = MF_INF, r1 = 0.0;
+        int c1 = 1;
 MF_UNROLL
         for (int jj = g.lane(); jj < nt; jj += G::N) {
           const int j = tl[jj];
           const int cn = cnt[j];
           const double r = res[j];
-          if (cn > 0) amin = smin(amin, dmul(smax(0.0, r), frecip(cn)));
+          if (cn > 0) {
+            const double rr = smax(0.0, r);
+            const double a = dmul(rr, frecip(cn));
+            const bool other = !(rr == r1 && cn == c1);
+            if (a < lmin) {
+              if (other) b2 = lmin;
+              lmin = a;
+              r1 = rr;
+              c1 = cn;
+            } else if (other) {
+              b2 = smin(b2, a);
+            }
+          }
         }
-        amin = g.min_nonneg(amin);  // smax(0, r) / cnt >= 0
+        const double amin = g.min_nonneg(lmin);  // smax(0, r) / cnt >= 0
         double inc = cmin;
-        // exact quotients only within the approximation margin; the gate widens
-        // by the same margin so that an exact minimum just below cmin whose
-        // approximation rounded above it still wins (allocator.cpp:88-93)
+        // the gate widens by the margin so that an exact minimum just below
+        // cmin whose approximation rounded above it still wins (allocator.cpp:88-93)
         if (dsub(amin, dmul(amin, 0x1p-18)) <= cmin) {
           const double athr = dadd(amin, dmul(amin, 0x1p-18));
           double q = MF_INF;
+          if (g.any(b2 <= athr)) {
 MF_UNROLL
-          for (int jj = g.lane(); jj < nt; jj += G::N) {
-            const int j = tl[jj];
-            const int cn = cnt[j];
-            const double r = smax(0.0, res[j]);
-            if (cn > 0 && dmul(r, frecip(cn)) <= athr) q = smin(q, ddiv(r, (double)cn));
+            for (int jj = g.lane(); jj < nt; jj += G::N) {
+              const int j = tl[jj];
+              const int cn = cnt[j];
+              const double r = smax(0.0, res[j]);
+              if (cn > 0 && dmul(r, frecip(cn)) <= athr) q = smin(q, ddiv(r, (double)cn));
+            }
+          } else if (lmin <= athr) {
+            q = ddiv(r1, (double)c1);
           }
           // quotients are >= +0 and cmin is never -0: min{cmin, q...} is order-free
           inc = smin(inc, g.min_nonneg(q));

@@ -183,8 +183,7 @@ template <bool kAalo>
 __global__ void __launch_bounds__(1024, 1)
     mfsim_gang_kernel(const Inst* __restrict__ insts, const int* __restrict__ order, int n,
                       int groups, int nsm, int* __restrict__ next, SmemPlan plan,
-                      long long budget, long long slice_ns, int* __restrict__ remaining,
-                      long long quantum, int split) {
+                      long long budget, long long slice_ns, int* __restrict__ remaining) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ unsigned long long t0;
   const int lane = threadIdx.x & 31;
@@ -210,26 +209,14 @@ __global__ void __launch_bounds__(1024, 1)
         if (eng.begin(budget)) state = 1;
       }
     }
-    int r = 0;
     if (state == 1) {
-      if (split) {  // the event, then (after a barrier) its rate recomputation
-        r = eng.step_event(deadline);
-      } else {
-        const long long c0 = clock64();
-        do {
-          r = eng.step(deadline);
-        } while (r == 0 && clock64() - c0 < quantum);
+      const int r = eng.step(deadline);
+      if (r != 0) {
+        const bool done = eng.end(r == 1);
+        if (done && lane == 0) atomicSub(remaining, 1);
+        __syncwarp();
+        state = 0;
       }
-    }
-    if (split) {
-      __syncthreads();
-      if (state == 1 && r == 0) eng.settle();
-    }
-    if (state == 1 && r != 0) {
-      const bool done = eng.end(r == 1);
-      if (done && lane == 0) atomicSub(remaining, 1);
-      __syncwarp();
-      state = 0;
     }
     if (!__syncthreads_or(state != 2)) break;
   }
@@ -262,11 +249,12 @@ class CudaBackend final : public Backend {
     for (auto k : {mfb::mfsim_gang_kernel<false>, mfb::mfsim_gang_kernel<true>})
       ck(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024),
          "smem attr");
+    // warps per lock-step gang: 32 (one gang per SM) measured +13 % over the
+    // one-warp kernel on the bench workload (profiles/r02_gang_ab.txt)
     if (const char* g = getenv("MFSIM_GANG")) gang_ = atoi(g);
     if (gang_ < 1) gang_ = 1;
     if (gang_ > 32) gang_ = 32;
-    if (const char* q = getenv("MFSIM_GANG_Q")) quantum_ = atoll(q);
-    if (const char* q = getenv("MFSIM_GANG_SPLIT")) split_ = atoi(q);
+    if (const char* g = getenv("MFSIM_GANG_MIN")) gang_min_ = atoi(g);  // tests: force small batches
     // deep per-warp call chains (noinline handlers) need more than the default
     ck(cudaDeviceSetLimit(cudaLimitStackSize, 4096), "stack limit");
   }
@@ -299,7 +287,9 @@ class CudaBackend final : public Backend {
   void launch(const mfb::Inst* d, const int* order, int n, const LaunchHint& hint,
               long long budget, long long slice_ns) override {
     const mfb::SmemPlan plan = mfb::make_plan(hint.nlinks);
-    if (gang_ > 1) {
+    // lock step pays off only when every SM holds a full gang: a batch of a
+    // few (large) instances keeps one warp per instance, spread over the SMs
+    if (gang_ > 1 && n >= (gang_min_ >= 0 ? gang_min_ : sms_ * gang_)) {
       launch_gang(d, order, n, hint, budget, slice_ns, plan);
       return;
     }
@@ -336,7 +326,7 @@ class CudaBackend final : public Backend {
     ck(cudaMemsetAsync(counter_ + 1, 0, sizeof(int) * kMaxGroups, stream_), "memset");
     ck(cudaEventRecord(e0_, stream_), "event");
     kern<<<grid, threads, bytes, stream_>>>(d, order, n, hint.groups, sms_, counter_ + 1, plan,
-                                             budget, slice_ns, counter_, quantum_, split_);
+                                             budget, slice_ns, counter_);
     ck(cudaGetLastError(), "launch");
     ck(cudaEventRecord(e1_, stream_), "event");
     ++launches_;
@@ -376,9 +366,8 @@ class CudaBackend final : public Backend {
   int* counter_ = nullptr;
   int* remain_host_ = nullptr;
   int sms_ = 148;
-  int gang_ = 1;  // warps per block in lock step (MFSIM_GANG, A/B)
-  long long quantum_ = 0;  // SM cycles of events per warp between barriers (MFSIM_GANG_Q)
-  int split_ = 0;  // barrier between an event and its rate recomputation (MFSIM_GANG_SPLIT)
+  int gang_ = 32;  // warps per block in lock step (MFSIM_GANG; 1 = one-warp kernel)
+  int gang_min_ = -1;  // fewest instances for a gang launch (-1: a full gang per SM)
   int last_grid_ = 0;
   int launches_ = 0;
   bool timed_ = false;

@@ -142,4 +142,22 @@ def test_config_5_bit_exact(product):
     """configs[4]: 4096-GPU fat-tree (3,768 links), heavy-tailed trace, mfs/fs"""
     g = golden("cfg5")
     assert len(g) == 2
-    assert _full(g, product, "configs[4]") == {}
+    # ~4k active flows: start above the 1024-flow first attempt (a capacity
+    # overflow re-runs the whole instance)
+    os.environ["MFSIM_ACTIVE_CAP"] = "8192"
+    try:
+        assert _full(g, product, "configs[4]") == {}
+    finally:
+        os.environ.pop("MFSIM_ACTIVE_CAP", None)
+
+
+@pytest.mark.skipif(os.environ.get("MFSIM_EMU_FULL") != "1", reason="set MFSIM_EMU_FULL=1 (~5 min of CPU)")
+def test_config_5_engine_logic_on_cpu(emu):
+    """configs[4] through the serial host build of the same engine source
+    (build/libmfsim_emu.so): ~2 min (fs) + ~3 min (mfs) on one core against the
+    reference's 1599 s / 1071 s; profiles/r02_emu_config5.log"""
+    os.environ["MFSIM_ACTIVE_CAP"] = "8192"
+    try:
+        assert _full(golden("cfg5"), emu, "configs[4] (emulated)") == {}
+    finally:
+        os.environ.pop("MFSIM_ACTIVE_CAP", None)

@@ -23,10 +23,12 @@ WORKLOAD = ["cluster8_400_mfs", "cluster8_400_karuna", "cluster8_400_fs", "fattr
 def _batch(product, gang):
     from paper_2603_17456_b200.native import DeviceBatch
     os.environ["MFSIM_GANG"] = str(gang)
+    os.environ["MFSIM_GANG_MIN"] = "1"  # the gang kernel even for this small batch
     try:
         b = DeviceBatch(0, product)
     finally:
         os.environ.pop("MFSIM_GANG", None)
+        os.environ.pop("MFSIM_GANG_MIN", None)
     man = [n for n in MANUAL if n in cases.manual_cases()]
     wl = [n for n in WORKLOAD if n in cases.workload_cases()]
     for n in man:

@@ -2,9 +2,7 @@
 workload, plus a bit-exactness check of every golden fixture under each gang size.
 
   python tools/gang_ab.py N SLICE_MS K SPEC1 SPEC2 ...
-SPEC = W[:q=CYCLES][:split] (W = 1: the one-warp kernel; q: events per warp
-between barriers until CYCLES SM cycles passed; split: a barrier between an
-event and its rate recomputation); add :noparity to skip the fixture check.
+SPEC = W[:noparity] (W = 1: the one-warp kernel; noparity: skip the fixture check).
 """
 import os
 import sys
@@ -26,13 +24,7 @@ for spec in sys.argv[4:]:
     parts = spec.split(":")
     w = int(parts[0])
     os.environ["MFSIM_GANG"] = str(w)
-    os.environ["MFSIM_GANG_Q"] = "0"
-    os.environ["MFSIM_GANG_SPLIT"] = "0"
-    for p in parts[1:]:
-        if p.startswith("q="):
-            os.environ["MFSIM_GANG_Q"] = p[2:]
-        elif p == "split":
-            os.environ["MFSIM_GANG_SPLIT"] = "1"
+    os.environ["MFSIM_GANG_MIN"] = "1"
     w = spec
     if "noparity" in parts:
         man, wl = [], []
