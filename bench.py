@@ -35,7 +35,7 @@ sys.path.insert(0, HERE)
 
 PEAKS = os.path.join(HERE, "MEASURED_PEAKS.json")
 HBM_FALLBACK = 6650.0
-NCU_SUMMARY = os.path.join(HERE, "profiles", "r01_ncu_engine_summary.json")
+NCU_SUMMARY = os.path.join(HERE, "profiles", "r02_ncu_gang_summary.json")
 
 
 def ncu_traffic(events_per_launch: float):
@@ -357,7 +357,7 @@ def main():
             "gpu_launches": args.steps,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                         "kernel": "mfsim_engine_kernel",
+                         "kernel": batch.last_kernel,
                          "algo_bytes_per_launch": algo_bytes / args.steps,
                          "traffic_source": traffic_src},
             "clocks": clk.summary(),

@@ -97,6 +97,9 @@ long long mfsim_dev_h2d_bytes(const mfsim_dev* d);
 long long mfsim_dev_d2h_bytes(const mfsim_dev* d);
 long long mfsim_dev_device_bytes(const mfsim_dev* d);
 int mfsim_dev_kernel_launches(const mfsim_dev* d);
+/* name of the kernel of the last launch ("mfsim_gang_kernel" for full batches,
+ * "mfsim_engine_kernel" otherwise); static storage */
+const char* mfsim_dev_last_kernel(const mfsim_dev* d);
 
 /* raw per-instance device counters (events, steps, ..., phase cycles in
  * profiling builds); returns the number written */

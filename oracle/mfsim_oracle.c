@@ -325,7 +325,7 @@ typedef struct {
   int has_horizon;
   double horizon;
   long maxtok, livelock;
-  int policy; /* 0 fs 1 sjf 2 edf 3 karuna 4 mfs 5 aalo (extension) */
+  int policy; /* 0 fs 1 sjf 2 edf 3 karuna 4 mfs 5 aalo 6 varys (extensions) */
   int K;
   double thr[MAXK];
   int prune;
@@ -953,6 +953,65 @@ static void decide(engine* e, classes* C) {
     qsort(k, A, sizeof(mkey), mfs_cmp);
     for (int i = 0; i < A; ++i) {
       if (i == 0 || k[i].band != k[i - 1].band || k[i].k1 != k[i - 1].k1) add_class(C);
+      C->ids[C->n++] = k[i].id;
+    }
+    free(k);
+  } else if (e->P.policy == 6) {
+    /* extension -- Varys-style SEBF + MADD coflow scheduling (no reference
+     * oracle; clairvoyant: it reads the remaining bytes). Coflow c as in Aalo
+     * (batch, target layer, stage; a flow without one is its own coflow).
+     * Effective bottleneck Gamma_c = max over links l of L_cl / capacity_l,
+     * L_cl = remaining bytes of c's active flows routed over l, summed in
+     * active order. One class per coflow, ordered by (Gamma_c, coflow key);
+     * MADD caps every member at remaining / Gamma_c (uncapped when Gamma_c is
+     * 0) so that, bandwidth permitting, a coflow's flows finish together;
+     * no backfilling beyond what the filling gives the lower classes. */
+    mkey* k = malloc(sizeof(mkey) * (A + 1));
+    for (int i = 0; i < A; ++i) {
+      flow* f = &FL(e, act[i]);
+      long c = aalo_idx(e, f);
+      mkey m = {i, 0, c >= 0 ? (double)c : 0x1p40 + act[i], (double)i, 0.0};
+      k[i] = m;
+    }
+    qsort(k, A, sizeof(mkey), mfs_cmp); /* members of a coflow, in active order */
+    double* L = calloc(e->F->nl + 1, sizeof(double));
+    double* gam = malloc(sizeof(double) * (A + 1));
+    for (int g0 = 0; g0 < A;) {
+      int g1 = g0 + 1;
+      while (g1 < A && k[g1].k1 == k[g0].k1) ++g1;
+      for (int i = g0; i < g1; ++i) {
+        flow* f = &FL(e, act[k[i].id]);
+        const int* rl = rlinks(e, f->route);
+        for (int q = 0; q < rlen(e, f->route); ++q) L[rl[q]] += f->rem;
+      }
+      double gmax = 0.0;
+      for (int i = g0; i < g1; ++i) {
+        flow* f = &FL(e, act[k[i].id]);
+        const int* rl = rlinks(e, f->route);
+        for (int q = 0; q < rlen(e, f->route); ++q) gmax = dmax(gmax, L[rl[q]] / e->F->cap[rl[q]]);
+      }
+      for (int i = g0; i < g1; ++i) {
+        flow* f = &FL(e, act[k[i].id]);
+        const int* rl = rlinks(e, f->route);
+        for (int q = 0; q < rlen(e, f->route); ++q) L[rl[q]] = 0.0;
+        gam[k[i].id] = gmax;
+      }
+      g0 = g1;
+    }
+    free(L);
+    C->caps = malloc(sizeof(double) * e->flows.n);
+    for (long i = 0; i < e->flows.n; ++i) C->caps[i] = NAN;
+    for (int i = 0; i < A; ++i) {
+      flow* f = &FL(e, act[i]);
+      long c = aalo_idx(e, f);
+      mkey m = {act[i], 0, gam[i], c >= 0 ? (double)c : 0x1p40 + act[i], 0.0};
+      k[i] = m;
+      if (gam[i] > 0.0) C->caps[act[i]] = f->rem / gam[i];
+    }
+    free(gam);
+    qsort(k, A, sizeof(mkey), mfs_cmp);
+    for (int i = 0; i < A; ++i) {
+      if (i == 0 || k[i].k1 != k[i - 1].k1 || k[i].k2 != k[i - 1].k2) add_class(C);
       C->ids[C->n++] = k[i].id;
     }
     free(k);
@@ -1952,7 +2011,7 @@ static int read_params(const kvcfg* c, params* P) {
   if (!pol) pol = "fs";
   P->policy = !strcmp(pol, "fs") ? 0 : !strcmp(pol, "sjf") ? 1 : !strcmp(pol, "edf") ? 2
             : !strcmp(pol, "karuna") ? 3 : !strcmp(pol, "mfs") ? 4
-            : !strcmp(pol, "aalo") ? 5 : -1;
+            : !strcmp(pol, "aalo") ? 5 : !strcmp(pol, "varys") ? 6 : -1;
   if (P->policy < 0) fail(2, "unknown policy");
   P->K = 8;
   if (P->policy == 5) { /* extension: Aalo D-CLAS queues, thresholds Q0 * E^i */

@@ -277,6 +277,7 @@ long long mfsim_dev_device_bytes(const mfsim_dev* d) {
   return d && d->batch ? static_cast<long long>(d->batch->device_bytes()) : 0;
 }
 int mfsim_dev_kernel_launches(const mfsim_dev* d) { return d ? d->be->kernel_launches() : 0; }
+const char* mfsim_dev_last_kernel(const mfsim_dev* d) { return d ? d->be->last_kernel() : ""; }
 
 int mfsim_dev_stats_get(const mfsim_dev* d, int i, mfsim_dev_stats* s) {
   if (!s) return fail(MFSIM_ERR_INVALID_ARG, "mfsim_dev_stats_get: NULL output");

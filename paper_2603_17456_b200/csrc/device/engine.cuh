@@ -1114,6 +1114,8 @@ MF_UNROLL
       ncls = group_classes(nd, nr, ncls);
     } else if (kAalo && pol == POL_AALO) {
       ncls = decide_aalo(A);
+    } else if (kAalo && pol == POL_VARYS) {
+      ncls = decide_varys(A, has_caps);
     } else {  // MFS arbitrate (rmlq.cpp:201-260)
       for (int p = g.lane(); p < A; p += G::N) {
         const int fid = I.a_fid[p];
@@ -1205,6 +1207,87 @@ MF_UNROLL
       I.s_k3[p] = 0;
     }
     g.sync();
+    const int n = sorted_subset(I.s_ord, SUB_ALL);
+    return group_classes(0, n, 0);
+  }
+
+  // Extension (no reference counterpart; oracle: oracle/mfsim_oracle.c decide,
+  // policy 6): Varys-style SEBF + MADD. Coflows as in Aalo (singleton coflow
+  // for a flow without a batch layer). Gamma_c = max over links of L_cl /
+  // capacity, L_cl = remaining bytes of c's members routed over l summed in
+  // active order; one class per coflow by (Gamma_c, coflow key); every member
+  // capped at remaining / Gamma_c (uncapped for Gamma_c = 0).
+  MF_NOINLINE int decide_varys(int A, bool* has_caps) {
+    int* __restrict__ ord = I.x_aux;  // members grouped by coflow, active order within
+    for (int p = g.lane(); p < A; p += G::N) {
+      const int fid = I.a_fid[p];
+      const int c = aalo_coflow(fid, I.f_batch[fid]);
+      I.s_k0[p] = c >= 0 ? (unsigned long long)c : (1ull << 40) + (unsigned long long)fid;
+      I.s_k1[p] = (unsigned long long)p;
+      I.s_k2[p] = 0;
+      I.s_k3[p] = 0;
+      ord[p] = p;
+    }
+    double* __restrict__ L = I.l_x;  // per-link scratch, zero between coflows
+    for (int p = g.lane(); p < A; p += G::N)
+      for (int k = 0; k < arn(p); ++k) L[arl(p, k)] = 0.0;
+    g.sync();
+    sort_ord(ord, A);
+    for (int g0 = 0; g0 < A;) {
+      const unsigned long long key = I.s_k0[ord[g0]];
+      int g1 = g0 + 1;
+      for (;;) {  // end of the coflow's run
+        const int i = g1 + g.lane();
+        const unsigned m = g.ballot(i >= A || I.s_k0[ord[i]] != key);
+        if (m) {
+          g1 += ctz32(m);
+          break;
+        }
+        g1 += G::N;
+      }
+      // link loads: members one after another, each over its route in parallel
+      for (int i = g0; i < g1; ++i) {
+        const int p = ord[i];
+        const int rn = arn(p);
+        const double rem = I.a_rem[p];
+        for (int k = g.lane(); k < rn; k += G::N) {
+          const int l = arl(p, k);
+          L[l] = dadd(L[l], rem);
+        }
+        g.sync();
+      }
+      double gm = 0.0;
+      for (int i = g0 + g.lane(); i < g1; i += G::N) {
+        const int p = ord[i];
+        const int rn = arn(p);
+        for (int k = 0; k < rn; ++k) {
+          const int l = arl(p, k);
+          gm = smax(gm, ddiv(L[l], I.cap[l]));
+        }
+      }
+      for (int m = G::N / 2; m > 0; m >>= 1) gm = smax(gm, g.shfl_xor(gm, m));
+      g.sync();
+      for (int i = g0 + g.lane(); i < g1; i += G::N) {
+        const int p = ord[i];
+        const int rn = arn(p);
+        for (int k = 0; k < rn; ++k) L[arl(p, k)] = 0.0;
+        I.s_cap[p] = gm;  // stash Gamma_c
+      }
+      g.sync();
+      g0 = g1;
+    }
+    for (int p = g.lane(); p < A; p += G::N) {
+      const int fid = I.a_fid[p];
+      const int c = aalo_coflow(fid, I.f_batch[fid]);
+      const double gam = I.s_cap[p];
+      I.s_k0[p] = 0;
+      I.s_k1[p] = dord(gam);
+      I.s_k2[p] = c >= 0 ? (unsigned long long)c : (1ull << 40) + (unsigned long long)fid;
+      I.s_k3[p] = 0;
+      I.s_cap[p] = gam > 0.0 ? ddiv(I.a_rem[p], gam) : MF_INF;
+    }
+    g.sync();
+    *has_caps = true;
     const int n = sorted_subset(I.s_ord, SUB_ALL);
     return group_classes(0, n, 0);
   }

@@ -31,7 +31,7 @@ class EmuBackend final : public Backend {
     if (n) std::memcpy(h, d, n);
   }
   void launch(const mfb::Inst* d, const int*, int n, const LaunchHint&, long long budget,
-              long long) override {
+              long long, int) override {
     for (int i = 0; i < n; ++i) {
       mfb::Inst local = d[i];
       mfb::Engine<mfb::SerialLanes> eng(local);
@@ -45,6 +45,7 @@ class EmuBackend final : public Backend {
   void set_stream(void*) override {}
   double last_kernel_ms() const override { return 0.0; }
   int kernel_launches() const override { return launches_; }
+  const char* last_kernel() const override { return "host-emulation"; }
 
  private:
   int launches_ = 0;

@@ -285,11 +285,12 @@ class CudaBackend final : public Backend {
     if (n) ck(cudaMemcpyAsync(h, d, n, cudaMemcpyDeviceToHost, stream_), "D2H");
   }
   void launch(const mfb::Inst* d, const int* order, int n, const LaunchHint& hint,
-              long long budget, long long slice_ns) override {
+              long long budget, long long slice_ns, int active) override {
     const mfb::SmemPlan plan = mfb::make_plan(hint.nlinks);
     // lock step pays off only when every SM holds a full gang: a batch of a
     // few (large) instances keeps one warp per instance, spread over the SMs
-    if (gang_ > 1 && n >= (gang_min_ >= 0 ? gang_min_ : sms_ * gang_)) {
+    if (active <= 0 || active > n) active = n;
+    if (gang_ > 1 && active >= (gang_min_ >= 0 ? gang_min_ : sms_ * gang_)) {
       launch_gang(d, order, n, hint, budget, slice_ns, plan);
       return;
     }
@@ -300,10 +301,14 @@ class CudaBackend final : public Backend {
                                                      plan.bytes),
        "occupancy");
     if (per_sm < 1) per_sm = 1;
+    // one wave of one-warp blocks lands round-robin over the SMs: with `active`
+    // instances left, ceil(active / SMs) warps per SM keep them on distinct SMs
+    const int want = (active + sms_ - 1) / sms_;
+    if (want < per_sm) per_sm = want > 0 ? want : 1;
     int grid = sms_ * per_sm;
-    if (n < grid) grid = n > 0 ? n : 1;
     ck(cudaMemsetAsync(counter_ + 1, 0, sizeof(int) * kMaxGroups, stream_), "memset");
     ck(cudaEventRecord(e0_, stream_), "event");
+    last_kernel_ = "mfsim_engine_kernel";
     kern<<<grid, 32, plan.bytes, stream_>>>(
         d, order, n, hint.groups, sms_, counter_ + 1, plan, budget, slice_ns, counter_);
     ck(cudaGetLastError(), "launch");
@@ -325,6 +330,7 @@ class CudaBackend final : public Backend {
     if (need < grid) grid = need > 0 ? need : 1;
     ck(cudaMemsetAsync(counter_ + 1, 0, sizeof(int) * kMaxGroups, stream_), "memset");
     ck(cudaEventRecord(e0_, stream_), "event");
+    last_kernel_ = "mfsim_gang_kernel";
     kern<<<grid, threads, bytes, stream_>>>(d, order, n, hint.groups, sms_, counter_ + 1, plan,
                                              budget, slice_ns, counter_);
     ck(cudaGetLastError(), "launch");
@@ -358,6 +364,7 @@ class CudaBackend final : public Backend {
   void set_stream(void* s) override { stream_ = static_cast<cudaStream_t>(s); }
   double last_kernel_ms() const override { return last_ms_; }
   int kernel_launches() const override { return launches_; }
+  const char* last_kernel() const override { return last_kernel_; }
 
  private:
   int device_;
@@ -367,6 +374,7 @@ class CudaBackend final : public Backend {
   int* remain_host_ = nullptr;
   int sms_ = 148;
   int gang_ = 32;  // warps per block in lock step (MFSIM_GANG; 1 = one-warp kernel)
+  const char* last_kernel_ = "";
   int gang_min_ = -1;  // fewest instances for a gang launch (-1: a full gang per SM)
   int last_grid_ = 0;
   int launches_ = 0;

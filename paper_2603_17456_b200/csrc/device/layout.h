@@ -22,7 +22,8 @@
 namespace mfb {
 
 enum : int { POL_FS = 0, POL_SJF = 1, POL_EDF = 2, POL_KARUNA = 3, POL_MFS = 4,
-             POL_AALO = 5 /* extension: no reference oracle (oracle/mfsim_oracle.c) */ };
+             POL_AALO = 5, /* extensions: no reference oracle (oracle/mfsim_oracle.c) */
+             POL_VARYS = 6 };
 enum : uint8_t { ST_REUSE = 0, ST_COLL = 1, ST_P2D = 2 };
 enum : uint8_t { FL_PENDING = 0, FL_ACTIVE = 1, FL_DONE = 2, FL_PRUNED = 3 };
 enum : uint8_t { BD_URGENT = 0, BD_EARLY = 1, BD_DEFERRED = 2, BD_SCAV = 3 };

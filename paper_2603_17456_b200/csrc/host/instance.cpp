@@ -969,7 +969,7 @@ void Batch::pack() {
       for (const Inst& d : desc_) {
         hint_.rmax = std::max(hint_.rmax, d.rmax);
         hint_.nlinks = std::max(hint_.nlinks, d.nlinks);
-        hint_.aalo = hint_.aalo || d.p.policy == mfb::POL_AALO;
+        hint_.aalo = hint_.aalo || d.p.policy == mfb::POL_AALO || d.p.policy == mfb::POL_VARYS;
       }
       in_bytes_ = c.in.off;
       st_bytes_ = c.st.off;
@@ -990,8 +990,8 @@ void Batch::pack() {
   std::vector<double> cost(n);
   for (int i = 0; i < n; ++i) {
     const Inst& d = desc_[i];
-    static const double factor[] = {1.0, 1.6, 1.1, 12.0, 2.5, 1.5};
-    const int pol = d.p.policy >= 0 && d.p.policy < 6 ? d.p.policy : 0;
+    static const double factor[] = {1.0, 1.6, 1.1, 12.0, 2.5, 1.5, 4.0};
+    const int pol = d.p.policy >= 0 && d.p.policy < 7 ? d.p.policy : 0;
     cost[i] = factor[pol] * (double(d.F_cap) + 2.0 * d.n_req);
   }
   // claim groups: one per policy, so that the warps sharing an SM run the same
@@ -1040,13 +1040,14 @@ void Batch::reset() {
   std::vector<int> zero(size(), 0);
   be_.h2d(phase_dev_, zero.data(), sizeof(int) * zero.size());
   be_.set_remaining(size());
+  remaining_ = size();
 }
 
 void Batch::launch(long long budget, long long slice_ns) {
-  be_.launch(desc_dev_, order_dev_, size(), hint_, budget, slice_ns);
+  be_.launch(desc_dev_, order_dev_, size(), hint_, budget, slice_ns, remaining_);
 }
 
-int Batch::remaining() { return be_.remaining(); }
+int Batch::remaining() { return remaining_ = be_.remaining(); }
 
 size_t Batch::output_bytes(int detail) const {
   size_t b = out_bytes_;
@@ -1113,9 +1114,15 @@ void Batch::run(int detail) {
   // scratch) stop with a capacity check; their bounds are raised and the
   // whole batch is re-packed and re-run, so the resident layout always holds
   // the final capacities (a later launch() re-simulates the same batch).
+  // Runs to completion as a series of time slices: each launch re-sizes its
+  // grid to the instances still running, so the long tail of a batch (the
+  // heaviest cells) ends up one instance per SM instead of sharing SMs with
+  // the warps that claimed them at the start.
+  long long slice_ns = 1000000000LL;
+  if (const char* e = std::getenv("MFSIM_RUN_SLICE_MS")) slice_ns = std::atoll(e) * 1000000LL;
   for (int attempt = 0; attempt < 16; ++attempt) {
     upload();
-    do launch(0);
+    do launch(0, slice_ns);
     while (remaining() > 0);
     download(detail);
     bool again = false;

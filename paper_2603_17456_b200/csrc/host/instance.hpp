@@ -38,7 +38,7 @@ struct LaunchHint {
   int rmax = 1;    // longest route of any instance
   int nlinks = 1;  // most links of any instance
   int groups = 1;  // claim groups (one per policy): order[n .. n+groups] holds their offsets
-  bool aalo = false;  // some instance runs the Aalo extension (kernel variant with its code)
+  bool aalo = false;  // some instance runs an extension policy (aalo / varys: the kernel variant with their code)
 };
 constexpr int kMaxGroups = 8;
 
@@ -56,14 +56,17 @@ class Backend {
   // order: device array, a permutation of [0, n) giving the claim order, in
   // hint.groups contiguous groups whose offsets follow at order[n..n+groups];
   // budget: events per instance in this launch (<= 0: run to completion)
+  // active: instances not finished yet (the host's last count; sizes the grid so
+  // that a few remaining instances land on distinct SMs)
   virtual void launch(const mfb::Inst* d_insts, const int* order, int n, const LaunchHint& hint,
-                      long long budget, long long slice_ns) = 0;
+                      long long budget, long long slice_ns, int active) = 0;
   virtual void set_remaining(int n) = 0;
   virtual int remaining() = 0;
   virtual void sync() = 0;
   virtual void set_stream(void* stream) = 0;
   virtual double last_kernel_ms() const = 0;
   virtual int kernel_launches() const = 0;
+  virtual const char* last_kernel() const = 0;
 };
 std::unique_ptr<Backend> make_backend(int device);
 
@@ -162,6 +165,7 @@ class Batch {
   mfb::Inst* desc_dev_ = nullptr;
   int* order_dev_ = nullptr;
   int* phase_dev_ = nullptr;
+  int remaining_ = 0;  // instances not finished at the last remaining() / reset()
   std::vector<int> order_;
   LaunchHint hint_;
   size_t in_bytes_ = 0, st_bytes_ = 0, out_bytes_ = 0;

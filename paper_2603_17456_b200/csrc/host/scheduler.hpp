@@ -15,9 +15,9 @@
 
 namespace mfh {
 
-enum class PolicyKind { FairShare, SJF, EDF, Karuna, MFS, Aalo };
+enum class PolicyKind { FairShare, SJF, EDF, Karuna, MFS, Aalo, Varys };
 
-// fs|sjf|edf|karuna|mfs, plus the extension aalo (no reference counterpart)
+// fs|sjf|edf|karuna|mfs, plus the extensions aalo and varys (no reference counterpart)
 PolicyKind parse_policy(const std::string& name);
 const char* policy_name(PolicyKind k);
 
@@ -85,6 +85,16 @@ class AaloScheduler : public Scheduler {
  private:
   int K_;
   double E_, Q0_;
+};
+
+// Extension: Varys-style SEBF + MADD (clairvoyant coflow scheduling). Coflows
+// as in Aalo; one class per coflow ordered by its effective bottleneck
+// Gamma = max over links of (remaining bytes over the link) / capacity; every
+// member capped at remaining / Gamma (MADD). Oracle: mfsim_oracle.c policy 6.
+class VarysScheduler : public Scheduler {
+ public:
+  const char* name() const override { return "varys"; }
+  PolicyKind kind() const override { return PolicyKind::Varys; }
 };
 
 std::unique_ptr<Scheduler> make_scheduler(PolicyKind kind, const Config& cfg);

@@ -103,6 +103,7 @@ class Native:
             "mfsim_dev_count": ([vp], i), "mfsim_dev_stats_get": ([vp, i, C.POINTER(DevStats)], i),
             "mfsim_dev_h2d_bytes": ([vp], ll), "mfsim_dev_d2h_bytes": ([vp], ll),
             "mfsim_dev_device_bytes": ([vp], ll), "mfsim_dev_kernel_launches": ([vp], i),
+            "mfsim_dev_last_kernel": ([vp], cp),
             "mfsim_dev_requests": ([vp, i, vp, vp, vp, vp, vp, vp, C.c_long], i),
             "mfsim_dev_flows": ([vp, i, vp, vp, vp, C.c_long], i),
             "mfsim_dev_coflows": ([vp, i, vp, vp, vp, C.c_long], i),
@@ -259,6 +260,10 @@ class DeviceBatch:
     @property
     def kernel_launches(self):
         return self.n.lib.mfsim_dev_kernel_launches(self.h)
+
+    @property
+    def last_kernel(self) -> str:
+        return self.n.lib.mfsim_dev_last_kernel(self.h).decode()
 
     def stats(self, i: int) -> DevStats:
         s = DevStats()

@@ -189,3 +189,69 @@ def test_aalo_device_matches_oracle(product):
         if d:
             bad[i] = d
     assert bad == {}
+
+
+# ---------------------------------------------------------------- varys
+# policy = varys: Varys-style SEBF + MADD (clairvoyant coflow scheduling):
+# coflows as in aalo; one class per coflow by its effective bottleneck
+# Gamma = max over links of remaining bytes over the link / capacity; members
+# capped at remaining / Gamma (MADD). Oracle: mfsim_oracle.c policy 6.
+
+def varys_cases():
+    out = {k: v.replace("policy = aalo", "policy = varys") for k, v in aalo_cases().items()
+           if "aalo." not in v}
+    c8 = open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "configs", "cluster8.conf")).read()
+    out["cluster8_300_rate12"] = c8 + "workload.request_count = 300\nworkload.rate_rps = 12\npolicy = varys\n"
+    return out
+
+
+@needs_oracle
+@pytest.mark.parametrize("name", sorted(varys_cases()))
+def test_varys_host_engine_matches_oracle(emu, name):
+    from paper_2603_17456_b200.native import run_config
+    text = varys_cases()[name]
+    assert "policy = varys" in text
+    want = ref.run_config(text, so=ref.ORACLE_SO)
+    got = run_config(text, lib=emu, detail=2)
+    assert diff(got, want) == []
+
+
+@needs_oracle
+@pytest.mark.parametrize("name", ["trio", "ingress", "egress", "single_request", "stall_zero",
+                                  "ticks", "tick_promotion"])
+def test_varys_manual_scenarios_match_oracle(emu, name):
+    from paper_2603_17456_b200.native import run_manual
+    import re
+    fn = getattr(cases, name)
+    spec = fn("mfs") if name in ("trio", "ingress", "egress") else fn()
+    spec = re.sub(r"^policy \w+", "policy varys", spec, flags=re.M)
+    assert "policy varys" in spec
+    assert diff(run_manual(spec, lib=emu), ref.run_manual(spec, so=ref.ORACLE_SO)) == []
+
+
+@needs_oracle
+def test_varys_differs_from_other_policies():
+    text = varys_cases()["cluster8_200"]
+    a = ref.run_config(text, so=ref.ORACLE_SO)
+    for p in POLICIES + ("aalo",):
+        b = ref.run_config(text.replace("policy = varys", f"policy = {p}"), so=ref.ORACLE_SO)
+        assert not bits_equal(a.flow_finish, b.flow_finish), p
+
+
+@pytest.mark.gpu
+def test_varys_device_matches_oracle(product):
+    from paper_2603_17456_b200 import sweep
+    from paper_2603_17456_b200.native import DeviceBatch
+    texts = list(varys_cases().values())
+    texts.append(sweep.sweep_config((0.8, 3, 1, "varys"), requests=400, lib=product))
+    b = DeviceBatch(0, product)
+    for t in texts:
+        b.add_config(t)
+    b.prepare()
+    b.run(2)
+    bad = {}
+    for i, t in enumerate(texts):
+        d = diff(b.result(i, 2, reports=True), ref.run_config(t, so=ref.ORACLE_SO))
+        if d:
+            bad[i] = d
+    assert bad == {}

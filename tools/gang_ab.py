@@ -2,7 +2,8 @@
 workload, plus a bit-exactness check of every golden fixture under each gang size.
 
   python tools/gang_ab.py N SLICE_MS K SPEC1 SPEC2 ...
-SPEC = W[:noparity] (W = 1: the one-warp kernel; noparity: skip the fixture check).
+SPEC = W[:noparity][:lib=PATH] (W = 1: the one-warp kernel; noparity: skip the
+fixture check; lib: an A/B build of the library instead of the product).
 """
 import os
 import sys
@@ -16,12 +17,15 @@ import bench  # noqa: E402
 import cases  # noqa: E402
 from parity import mismatches  # noqa: E402
 from paper_2603_17456_b200 import sweep  # noqa: E402
-from paper_2603_17456_b200.native import DeviceBatch, product  # noqa: E402
+from paper_2603_17456_b200.native import DeviceBatch, Native, product  # noqa: E402
 
 n, slice_ms, k = int(sys.argv[1]), float(sys.argv[2]), int(sys.argv[3])
-lib = product()
 for spec in sys.argv[4:]:
     parts = spec.split(":")
+    lib = product()
+    for p in parts:
+        if p.startswith("lib="):
+            lib = Native(p[4:])
     w = int(parts[0])
     os.environ["MFSIM_GANG"] = str(w)
     os.environ["MFSIM_GANG_MIN"] = "1"
