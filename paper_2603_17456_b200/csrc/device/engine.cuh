@@ -114,12 +114,6 @@ MF_FN int popc32(unsigned m) { return __builtin_popcount(m); }
 #else
 #define MF_SH(ptr) ((void)0)
 #endif
-// ... and global memory (LDG/STG instead of generic LD/ST)
-#if defined(__CUDACC__) && !defined(MF_NO_GL)
-#define MF_GL(ptr) __builtin_assume(__isGlobal(ptr))
-#else
-#define MF_GL(ptr) ((void)0)
-#endif
 
 // 1/n correctly rounded for small n (exact table), else a division
 #if defined(__CUDACC__)
@@ -1779,24 +1773,7 @@ MF_UNROLL
       MF_SH(tl);
       MF_SH(sat);
       MF_SH(frz);
-    } else {
-      MF_GL(res);
-      MF_GL(cnt);
-      MF_GL(mb);
-      MF_GL(mend);
-      MF_GL(tl);
-      MF_GL(sat);
-      MF_GL(frz);
     }
-    MF_GL(ord);
-    MF_GL(afid);
-    MF_GL(asl);
-    MF_GL(arnp);
-    MF_GL(rate);
-    MF_GL(capv);
-    MF_GL(slink);
-    MF_GL(scap);
-    MF_GL(mem);
     MF_TIC(q0);
     if (I.p.policy == POL_MFS) {  // rate-map insertion order (load_fraction)
       int* __restrict__ hk = I.h_keys;
