@@ -1470,7 +1470,48 @@ MF_UNROLL
       }
     }
     g.sync();
-    // per-link demand summed in deadline_ids (= active) order (baselines.cpp:112-118):
+    // per-link demand summed in deadline_ids (= active) order (baselines.cpp:112-118)
+#if defined(MF_KARUNA_BUCKET)
+    // entries (link, want) in flow order, stably bucketed by link; one lane
+    // sums one link's bucket in order
+    {
+      int n = 0;
+      for (int base = 0; base < nd; base += G::N) {
+        const int i = base + g.lane();
+        int c = 0, p = 0;
+        double want = MF_INF;
+        if (i < nd) {
+          p = I.s_ord[i];
+          want = I.s_cap[p];
+          if (want < MF_INF) c = arn(p);
+        }
+        int tot;
+        const int off = g.excl_scan(c, &tot);
+        for (int k = 0; k < c; ++k) {
+          I.x_seg[n + off + k] = entry_key(p, k);
+          I.x_val[n + off + k] = want;
+          I.x_hi[n + off + k] = 0;
+          I.x_aux[n + off + k] = 0;
+        }
+        n += tot;
+      }
+      g.sync();
+      if (n > I.X_cap) {
+        fail(ERR_INTERNAL, CHK_CAP_SCRATCH);
+        return;
+      }
+      const int nt = bucket_by_link(n);
+      for (int j = g.lane(); j < nt; j += G::N) {
+        int e0, e1;
+        const int l = bucket_at(j, &e0, &e1);
+        double dm = 0.0;
+        for (int a = e0; a < e1; ++a) dm = dadd(dm, I.y_val[a]);
+        I.l_x[l] = dm;
+      }
+      g.sync();
+      bucket_release(nt);
+    }
+#else
     // flows one after another, each adding to its (distinct) route links in parallel
     for (int i0 = 0; i0 < nd; i0 += G::N) {
       const int i = i0 + g.lane();
@@ -1494,6 +1535,7 @@ MF_UNROLL
         g.sync();
       }
     }
+#endif
     for (int i = g.lane(); i < nd; i += G::N) {
       const int p = I.s_ord[i];
       const double want = I.s_cap[p];
