@@ -118,6 +118,7 @@ def _full(g, product, label):
 
 @pytest.mark.gpu
 @FULL
+@pytest.mark.timeout(0)
 def test_config_3_bit_exact(product):
     """configs[2]: ft128 (1024 GPUs), 100k requests, fs/sjf/edf/mfs x seeds 1-3
     (12 instances in one launch, one warp each; ~25 min)"""
@@ -128,6 +129,7 @@ def test_config_3_bit_exact(product):
 
 @pytest.mark.gpu
 @pytest.mark.skipif(os.environ.get("MFSIM_FULL_PARITY_KARUNA") != "1", reason="set MFSIM_FULL_PARITY_KARUNA=1")
+@pytest.mark.timeout(0)
 def test_config_3_karuna_bit_exact(product):
     """configs[2], Karuna x seeds 1-3: ~24M events at ~240 us each on one warp
     (~1.6 h) -- longer than one 60-minute box call"""
@@ -138,6 +140,7 @@ def test_config_3_karuna_bit_exact(product):
 
 @pytest.mark.gpu
 @FULL
+@pytest.mark.timeout(0)
 def test_config_5_bit_exact(product):
     """configs[4]: 4096-GPU fat-tree (3,768 links), heavy-tailed trace, mfs/fs"""
     g = golden("cfg5")
@@ -152,6 +155,7 @@ def test_config_5_bit_exact(product):
 
 
 @pytest.mark.skipif(os.environ.get("MFSIM_EMU_FULL") != "1", reason="set MFSIM_EMU_FULL=1 (~5 min of CPU)")
+@pytest.mark.timeout(0)
 def test_config_5_engine_logic_on_cpu(emu):
     """configs[4] through the serial host build of the same engine source
     (build/libmfsim_emu.so): ~2 min (fs) + ~3 min (mfs) on one core against the
