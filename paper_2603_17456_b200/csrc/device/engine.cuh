@@ -3408,6 +3408,11 @@ MF_UNROLL
         I.out[OUT_EVENTS] = s.events;  // progress, visible while suspended
         I.out[OUT_STEPS] = s.steps;
         I.out[OUT_ALGO_BYTES] = s.algo_bytes;
+#if defined(MF_PROF)
+        I.out[OUT_ROUNDS] = s.rounds;
+        I.out[OUT_MAXACTIVE] = s.max_active;
+        for (int k = 0; k < 32; ++k) I.out[OUT_CY_NEXT + k] = s.cy[k];
+#endif
       }
       pool_copy(false, s.n_ev);
       return false;
