@@ -151,12 +151,6 @@ struct Sc {
   unsigned long long seq;
   long long events, steps, streak, pushes, algo_bytes, classes, rounds;
   long long stop_at;  // event count at which this launch suspends
-  // resumable slot filling (alloc_begin / alloc_unit)
-  int ph;  // 0: at an event boundary, 1: the rate recomputation is in progress
-  int a_ncls, a_c, a_nu, a_nt, a_ncap;
-  bool a_caps;
-  double a_R, a_cmn;
-  long long a_rounds, a_bytes;
   int n_flows, n_batches, n_coflows, n_active, n_ev;
   int rp_top, pp_top, cm_top;
   int next_arr;
@@ -1792,52 +1786,13 @@ MF_UNROLL
     for (int k = 0; k < rn; ++k) g.atomic_add(&cnt[sl[k]], v);
   }
 
-  // Strict-priority filling over the link slots, as resumable units: the
-  // lock-step gang advances one unit per barrier (a run of singleton classes
-  // plus the next multi-flow class's setup, or one filling round), so that the
-  // warps of a gang wait for the slowest ROUND rather than the slowest event.
-  // alloc_begin + alloc_unit until it returns true == allocate_slots.
-  MF_NOINLINE void alloc_begin(int ncls, bool has_caps) {
+  template <bool kLinksOnChip>
+  MF_NOINLINE void allocate_slots(int ncls, bool has_caps) {
     const int A = s.n_active;
+    const int RM = I.rmax;
     const int hw = s.sl_hw;
     int* __restrict__ ord = I.s_ord;
     const int* __restrict__ afid = I.a_fid;
-    double* __restrict__ res = I.sl_res;
-    int* __restrict__ cnt = I.sl_cnt;
-    const double* __restrict__ capv = I.cap;
-    const unsigned short* __restrict__ slink = I.sl_link;
-    MF_TIC(q0);
-    if (I.p.policy == POL_MFS) {  // rate-map insertion order (load_fraction)
-      int* __restrict__ hk = I.h_keys;
-      int* __restrict__ hidx = I.f_hidx;
-      for (int i = g.lane(); i < A; i += G::N) {
-        const int fid = afid[ord[i]];
-        hk[i] = fid;
-        hidx[fid] = i;
-      }
-      s.h_n = A;
-      s.h_ready = 0;
-    }
-    // residual = capacity on every slot (allocator.cpp:36-37), counts zero
-    for (int j = g.lane(); j < hw; j += G::N) {
-      res[j] = capv[slink[j]];
-      cnt[j] = 0;
-    }
-    g.sync();
-    MF_TOC(OUT_CY_SUB + 0, q0);
-    s.a_ncls = ncls;
-    s.a_caps = has_caps;
-    s.a_c = 0;
-    s.a_nu = 0;
-    s.a_rounds = 0;
-    s.a_bytes = 0;
-  }
-
-  template <bool kLinksOnChip>
-  MF_NOINLINE bool alloc_unit() {
-    const int A = s.n_active;
-    const int RM = I.rmax;
-    int* __restrict__ ord = I.s_ord;
     const unsigned short* __restrict__ asl = I.a_sl;
     const uint8_t* __restrict__ arnp = I.a_rn;
     double* __restrict__ res = I.sl_res;
@@ -1861,14 +1816,126 @@ MF_UNROLL
       MF_SH(sat);
       MF_SH(frz);
     }
-    const int ncls = s.a_ncls;
-    const bool has_caps = s.a_caps;
-    long long rounds = s.a_rounds, bytes = s.a_bytes;
-    int c = s.a_c;
-    if (s.a_nu > 0) {  // one round of the multi-flow class c
-      int nu = s.a_nu, nt = s.a_nt, ncap = s.a_ncap;
-      double R = s.a_R, cmn = s.a_cmn;
-      {
+    MF_TIC(q0);
+    if (I.p.policy == POL_MFS) {  // rate-map insertion order (load_fraction)
+      int* __restrict__ hk = I.h_keys;
+      int* __restrict__ hidx = I.f_hidx;
+      for (int i = g.lane(); i < A; i += G::N) {
+        const int fid = afid[ord[i]];
+        hk[i] = fid;
+        hidx[fid] = i;
+      }
+      s.h_n = A;
+      s.h_ready = 0;
+    }
+    // residual = capacity on every slot (allocator.cpp:36-37), counts zero
+    for (int j = g.lane(); j < hw; j += G::N) {
+      res[j] = capv[slink[j]];
+      cnt[j] = 0;
+    }
+    g.sync();
+    MF_TOC(OUT_CY_SUB + 0, q0);
+    long long rounds = 0, bytes = 0;
+    for (int c = 0; c < ncls; ++c) {
+      const int o0 = I.s_cls[c], o1 = I.s_cls[c + 1];
+      const int n = o1 - o0;
+      if (n == 1) {  // singleton: bottleneck residual, capped (allocator.cpp:42-59)
+        const int p = ord[o0];
+        const int rn = arnp[p];
+        double r = MF_INF;
+        if (has_caps) {
+          const double cp = scap[p];
+          if (cp < MF_INF) r = smax(0.0, cp);
+        }
+        double mine = MF_INF;
+        for (int k = g.lane(); k < rn; k += G::N) mine = smin(mine, smax(0.0, res[asl[p * RM + k]]));
+        mine = g.min_nonneg(mine);  // smax(0, residual) >= 0
+        r = smin(r, mine);
+        g.sync();
+        for (int k = g.lane(); k < rn; k += G::N) {
+          const int j = asl[p * RM + k];
+          res[j] = dsub(res[j], r);
+        }
+        if (g.leader()) rate[p] = r;
+        g.sync();
+        bytes += 20LL * rn + 12;
+        continue;
+      }
+      // multi-flow class (allocator.cpp:61-121). Every unfrozen member has
+      // received the same sequence of increments from 0, so they share one
+      // rate R; a member's rate is R at the round it freezes. Per round:
+      //   inc = max(min(min_j max(0,res_j)/cnt_j, capmin - R), 0)
+      //   R += inc; res_j -= inc * cnt_j on slots with unfrozen members
+      //   freeze members of slots whose residual fell to <= 1e-12 * capacity
+      //   and members with R >= cap - eps. capmin - R is min_p(cap_p - R)
+      //   (rounding is monotone); the capped unfrozen members are one list,
+      //   compacted and re-minimised by the cap pass of every round.
+      MF_TIC(q1);
+      int nt = 0, ncap = 0;
+      double cmn = MF_INF;
+      for (int w = g.lane(); w < ((A + 31) >> 5); w += G::N) frz[w] = 0u;
+      for (int base = 0; base < n; base += G::N) {
+        const int i = base + g.lane();
+        int p = 0, rn = 0;
+        bool capped = false;
+        if (i < n) {
+          p = ord[o0 + i];
+          rn = arnp[p];
+          if (has_caps) capped = scap[p] < MF_INF;
+        }
+        for (int k = 0; k < RM; ++k) {
+          bool first = false;
+          int j = 0;
+          if (k < rn) {
+            j = asl[p * RM + k];
+            first = g.atomic_add(&cnt[j], 1) == 0;
+          }
+          const unsigned m = g.ballot(first);
+          if (first) tl[nt + popc32(m & g.lanemask_lt())] = (unsigned short)j;
+          nt += popc32(m);
+        }
+        const unsigned mc = g.ballot(capped);
+        if (capped) {  // (cap, position) of the capped members
+          const int slot = ncap + popc32(mc & g.lanemask_lt());
+          const double cp = smax(0.0, scap[p]);
+          I.x_hi[slot] = dbits(cp);
+          I.x_lo[slot] = (unsigned long long)p;
+          cmn = smin(cmn, cp);
+        }
+        ncap += popc32(mc);
+      }
+      cmn = g.min_nonneg(cmn);  // smax(0, cap) >= 0
+      g.sync();
+      {  // slot -> member incidence: extents from the counts, atomic fill
+        int off = 0;
+        for (int base = 0; base < nt; base += G::N) {
+          const int jj = base + g.lane();
+          int c0 = 0, j = 0;
+          if (jj < nt) {
+            j = tl[jj];
+            c0 = cnt[j];
+          }
+          int tot;
+          const int o = g.excl_scan(c0, &tot);
+          if (jj < nt) {
+            mb[j] = off + o;
+            mend[j] = off + o;
+          }
+          off += tot;
+        }
+        g.sync();
+        for (int i = g.lane(); i < n; i += G::N) {
+          const int p = ord[o0 + i];
+          const int rn = arnp[p];
+          for (int k = 0; k < rn; ++k) mem[g.atomic_add(&mend[asl[p * RM + k]], 1)] = (unsigned short)p;
+        }
+        g.sync();
+      }
+      MF_TOC(OUT_CY_SUB + 1, q1);
+      if (nt > s.max_touch) s.max_touch = nt;
+      int nu = n;
+      double R = 0.0;
+      while (nu > 0) {
         ++rounds;
         MF_TIC(q2);
         const double cmin = ncap > 0 ? dsub(cmn, R) : MF_INF;
@@ -2022,148 +2089,18 @@ MF_UNROLL
         bytes += 32LL * nt + 24LL * frozen;
         if (frozen == 0) {
           fail(ERR_INTERNAL, CHK_NO_PROGRESS);
-          s.a_nu = 0;
-          return true;
+          return;
         }
         nu -= frozen;
         nt = nt2;
       }
-      if (nu > 0) {
-        s.a_nu = nu;
-        s.a_nt = nt;
-        s.a_ncap = ncap;
-        s.a_R = R;
-        s.a_cmn = cmn;
-        s.a_rounds = rounds;
-        s.a_bytes = bytes;
-        return false;
-      }
       // slot counts of this class are back to zero (every member froze)
       for (int jj = g.lane(); jj < nt; jj += G::N) cnt[tl[jj]] = 0;
       g.sync();
-      s.a_nu = 0;
-      ++c;
     }
-    for (; c < ncls; ++c) {
-      const int o0 = I.s_cls[c], o1 = I.s_cls[c + 1];
-      const int n = o1 - o0;
-      if (n == 0) continue;  // empty class (allocator.cpp:42)
-      if (n == 1) {  // singleton: bottleneck residual, capped (allocator.cpp:42-59)
-        const int p = ord[o0];
-        const int rn = arnp[p];
-        double r = MF_INF;
-        if (has_caps) {
-          const double cp = scap[p];
-          if (cp < MF_INF) r = smax(0.0, cp);
-        }
-        double mine = MF_INF;
-        for (int k = g.lane(); k < rn; k += G::N) mine = smin(mine, smax(0.0, res[asl[p * RM + k]]));
-        mine = g.min_nonneg(mine);  // smax(0, residual) >= 0
-        r = smin(r, mine);
-        g.sync();
-        for (int k = g.lane(); k < rn; k += G::N) {
-          const int j = asl[p * RM + k];
-          res[j] = dsub(res[j], r);
-        }
-        if (g.leader()) rate[p] = r;
-        g.sync();
-        bytes += 20LL * rn + 12;
-        continue;
-      }
-      // multi-flow class (allocator.cpp:61-121). Every unfrozen member has
-      // received the same sequence of increments from 0, so they share one
-      // rate R; a member's rate is R at the round it freezes. Per round:
-      //   inc = max(min(min_j max(0,res_j)/cnt_j, capmin - R), 0)
-      //   R += inc; res_j -= inc * cnt_j on slots with unfrozen members
-      //   freeze members of slots whose residual fell to <= 1e-12 * capacity
-      //   and members with R >= cap - eps. capmin - R is min_p(cap_p - R)
-      //   (rounding is monotone); the capped unfrozen members are one list,
-      //   compacted and re-minimised by the cap pass of every round.
-      MF_TIC(q1);
-      int nt = 0, ncap = 0;
-      double cmn = MF_INF;
-      for (int w = g.lane(); w < ((A + 31) >> 5); w += G::N) frz[w] = 0u;
-      for (int base = 0; base < n; base += G::N) {
-        const int i = base + g.lane();
-        int p = 0, rn = 0;
-        bool capped = false;
-        if (i < n) {
-          p = ord[o0 + i];
-          rn = arnp[p];
-          if (has_caps) capped = scap[p] < MF_INF;
-        }
-        for (int k = 0; k < RM; ++k) {
-          bool first = false;
-          int j = 0;
-          if (k < rn) {
-            j = asl[p * RM + k];
-            first = g.atomic_add(&cnt[j], 1) == 0;
-          }
-          const unsigned m = g.ballot(first);
-          if (first) tl[nt + popc32(m & g.lanemask_lt())] = (unsigned short)j;
-          nt += popc32(m);
-        }
-        const unsigned mc = g.ballot(capped);
-        if (capped) {  // (cap, position) of the capped members
-          const int slot = ncap + popc32(mc & g.lanemask_lt());
-          const double cp = smax(0.0, scap[p]);
-          I.x_hi[slot] = dbits(cp);
-          I.x_lo[slot] = (unsigned long long)p;
-          cmn = smin(cmn, cp);
-        }
-        ncap += popc32(mc);
-      }
-      cmn = g.min_nonneg(cmn);  // smax(0, cap) >= 0
-      g.sync();
-      {  // slot -> member incidence: extents from the counts, atomic fill
-        int off = 0;
-        for (int base = 0; base < nt; base += G::N) {
-          const int jj = base + g.lane();
-          int c0 = 0, j = 0;
-          if (jj < nt) {
-            j = tl[jj];
-            c0 = cnt[j];
-          }
-          int tot;
-          const int o = g.excl_scan(c0, &tot);
-          if (jj < nt) {
-            mb[j] = off + o;
-            mend[j] = off + o;
-          }
-          off += tot;
-        }
-        g.sync();
-        for (int i = g.lane(); i < n; i += G::N) {
-          const int p = ord[o0 + i];
-          const int rn = arnp[p];
-          for (int k = 0; k < rn; ++k) mem[g.atomic_add(&mend[asl[p * RM + k]], 1)] = (unsigned short)p;
-        }
-        g.sync();
-      }
-      MF_TOC(OUT_CY_SUB + 1, q1);
-      if (nt > s.max_touch) s.max_touch = nt;
-      s.a_c = c;
-      s.a_nu = n;
-      s.a_nt = nt;
-      s.a_ncap = ncap;
-      s.a_cmn = cmn;
-      s.a_R = 0.0;
-      s.a_rounds = rounds;
-      s.a_bytes = bytes;
-      return false;
-    }
-    s.a_c = c;
     s.classes += ncls;
     s.rounds += rounds;
     s.algo_bytes += bytes;
-    return true;
-  }
-
-  template <bool kLinksOnChip>
-  MF_NOINLINE void allocate_slots(int ncls, bool has_caps) {
-    alloc_begin(ncls, has_caps);
-    while (!alloc_unit<kLinksOnChip>()) {
-    }
   }
 
   // engine.cpp:278-293
@@ -2178,12 +2115,6 @@ MF_UNROLL
     allocate(ncls, has_caps);
     MF_TOC(OUT_CY_ALLOC, t1);
     if (s.err) return;
-    resched();
-  }
-
-  // changed rates -> new completion events, pushed in active_ order
-  // (engine.cpp:281-291)
-  MF_NOINLINE void resched() {
     MF_TIC(t2);
     const int A = s.n_active;
     const unsigned long long seq0 = s.seq;
@@ -3159,7 +3090,6 @@ MF_UNROLL
     s.prev_t = -1.0;
     s.seq = (unsigned long long)seq0;
     s.events = s.steps = s.streak = s.pushes = s.algo_bytes = s.classes = s.rounds = 0;
-    s.ph = 0;
     s.n_flows = n_flows0;
     s.n_batches = n_batches0;
     s.n_coflows = n_coflows0;
@@ -3264,41 +3194,17 @@ MF_UNROLL
 
   // one iteration of Engine::run's loop (engine.cpp:598-655): 0 = go on,
   // 1 = finished (or failed), 2 = suspend (event budget or deadline reached)
-  // While the rate recomputation of the previous event is in progress (ph),
-  // a step is one filling unit instead.
   MF_NOINLINE int step(unsigned long long deadline_ns) {
-    if (s.ph) {
-      if (chip ? alloc_unit<true>() : alloc_unit<false>()) finish_rates();
-      return s.err ? 1 : 0;
-    }
     const int r = step_event(deadline_ns);
     if (r == 0) settle();
     return s.err ? 1 : r;
   }
-  // The rate recomputation that closes an event (engine.cpp:651-654,
-  // recompute_rates engine.cpp:278-293): decide, then the filling -- over the
-  // link slots as resumable units (the first one here, the rest by the next
-  // steps), else in one piece -- then the completion events.
+  // the rate recomputation that closes an event (engine.cpp:651-654)
   MF_NOINLINE void settle() {
-    if (!s.dirty || s.err) return;
-    bool has_caps = false;
-    const int ncls = decide(&has_caps);
-    if (s.err) return;
-    ++s.steps;
-    if (I.TS_cap > 0 && s.n_unslotted == 0) {
-      alloc_begin(ncls, has_caps);
-      s.ph = 1;
-      if (chip ? alloc_unit<true>() : alloc_unit<false>()) finish_rates();
-    } else {
-      allocate_generic(ncls, has_caps);
-      if (!s.err) resched();
+    if (s.dirty && !s.err) {
+      recompute_rates();
       s.dirty = 0;
     }
-  }
-  MF_FN void finish_rates() {
-    if (!s.err) resched();
-    s.ph = 0;
-    s.dirty = 0;
   }
   // the event itself: pop, advance, dispatch; leaves s.dirty for settle()
   MF_NOINLINE int step_event(unsigned long long deadline_ns) {
@@ -3408,6 +3314,10 @@ MF_UNROLL
         I.out[OUT_EVENTS] = s.events;  // progress, visible while suspended
         I.out[OUT_STEPS] = s.steps;
         I.out[OUT_ALGO_BYTES] = s.algo_bytes;
+        I.out[OUT_NFLOWS] = s.n_flows;  // sizes of the partial state (a cut)
+        I.out[OUT_NBATCHES] = s.n_batches;
+        I.out[OUT_NCOFLOWS] = s.n_coflows;
+        I.out[OUT_PRUNED] = s.pruned;
 #if defined(MF_PROF)
         I.out[OUT_ROUNDS] = s.rounds;
         I.out[OUT_MAXACTIVE] = s.max_active;
