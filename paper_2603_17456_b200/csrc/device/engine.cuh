@@ -1470,48 +1470,7 @@ MF_UNROLL
       }
     }
     g.sync();
-    // per-link demand summed in deadline_ids (= active) order (baselines.cpp:112-118)
-#if defined(MF_KARUNA_BUCKET)
-    // entries (link, want) in flow order, stably bucketed by link; one lane
-    // sums one link's bucket in order
-    {
-      int n = 0;
-      for (int base = 0; base < nd; base += G::N) {
-        const int i = base + g.lane();
-        int c = 0, p = 0;
-        double want = MF_INF;
-        if (i < nd) {
-          p = I.s_ord[i];
-          want = I.s_cap[p];
-          if (want < MF_INF) c = arn(p);
-        }
-        int tot;
-        const int off = g.excl_scan(c, &tot);
-        for (int k = 0; k < c; ++k) {
-          I.x_seg[n + off + k] = entry_key(p, k);
-          I.x_val[n + off + k] = want;
-          I.x_hi[n + off + k] = 0;
-          I.x_aux[n + off + k] = 0;
-        }
-        n += tot;
-      }
-      g.sync();
-      if (n > I.X_cap) {
-        fail(ERR_INTERNAL, CHK_CAP_SCRATCH);
-        return;
-      }
-      const int nt = bucket_by_link(n);
-      for (int j = g.lane(); j < nt; j += G::N) {
-        int e0, e1;
-        const int l = bucket_at(j, &e0, &e1);
-        double dm = 0.0;
-        for (int a = e0; a < e1; ++a) dm = dadd(dm, I.y_val[a]);
-        I.l_x[l] = dm;
-      }
-      g.sync();
-      bucket_release(nt);
-    }
-#else
+    // per-link demand summed in deadline_ids (= active) order (baselines.cpp:112-118):
     // flows one after another, each adding to its (distinct) route links in parallel
     for (int i0 = 0; i0 < nd; i0 += G::N) {
       const int i = i0 + g.lane();
@@ -1535,7 +1494,6 @@ MF_UNROLL
         g.sync();
       }
     }
-#endif
     for (int i = g.lane(); i < nd; i += G::N) {
       const int p = I.s_ord[i];
       const double want = I.s_cap[p];
@@ -1786,6 +1744,100 @@ MF_UNROLL
     for (int k = 0; k < rn; ++k) g.atomic_add(&cnt[sl[k]], v);
   }
 
+#if defined(MF_CAP_SORT)
+  // Ascending sort of the capped entries (x_hi = cap bits, x_lo = active
+  // position) of one class, n <= kCapSort: a bitonic network over registers
+  // (8 entries per lane; lane-crossing stages by shuffle, register-crossing
+  // stages by static pairs). Caps are >= 0, so their bit patterns order like
+  // the values; equal caps may come out in any order (they freeze together).
+  static constexpr int kCapSort = 8 * G::N;
+  MF_FN static bool kv_gt(unsigned long long ha, unsigned la, unsigned long long hb, unsigned lb) {
+    return ha > hb || (ha == hb && la > lb);
+  }
+  MF_NOINLINE void sort_caps(int n) {
+    unsigned long long* __restrict__ xh = I.x_hi;
+    unsigned long long* __restrict__ xl = I.x_lo;
+    if (G::N == 1) {  // serial build: insertion sort
+      for (int i = 1; i < n; ++i) {
+        const unsigned long long h = xh[i], l = xl[i];
+        int j = i - 1;
+        while (j >= 0 && kv_gt((unsigned long long)xh[j], (unsigned)xl[j], h, (unsigned)l)) {
+          xh[j + 1] = xh[j];
+          xl[j + 1] = xl[j];
+          --j;
+        }
+        xh[j + 1] = h;
+        xl[j + 1] = l;
+      }
+      return;
+    }
+    constexpr int E = 8;
+    int n2 = G::N;
+    while (n2 < n) n2 <<= 1;
+    const int nm = n2 / G::N;
+    unsigned long long h[E];
+    unsigned lo[E];
+#pragma unroll
+    for (int m = 0; m < E; ++m) {
+      const int i = m * G::N + g.lane();
+      h[m] = i < n ? xh[i] : ~0ull;
+      lo[m] = i < n ? (unsigned)xl[i] : ~0u;
+    }
+#define MF_CS(a, b)                                                   \
+  if ((b) < nm) {                                                      \
+    const bool up = (((a)*G::N + g.lane()) & k) == 0;                  \
+    if (kv_gt(h[a], lo[a], h[b], lo[b]) == up) {                       \
+      const unsigned long long th = h[a];                              \
+      const unsigned tl_ = lo[a];                                      \
+      h[a] = h[b];                                                     \
+      lo[a] = lo[b];                                                   \
+      h[b] = th;                                                       \
+      lo[b] = tl_;                                                     \
+    }                                                                  \
+  }
+    for (int k = 2; k <= n2; k <<= 1) {
+      for (int j = k >> 1; j > 0; j >>= 1) {
+        if (j >= G::N) {
+          const int jm = j / G::N;
+          if (jm == 1) {
+            MF_CS(0, 1) MF_CS(2, 3) MF_CS(4, 5) MF_CS(6, 7)
+          } else if (jm == 2) {
+            MF_CS(0, 2) MF_CS(1, 3) MF_CS(4, 6) MF_CS(5, 7)
+          } else {
+            MF_CS(0, 4) MF_CS(1, 5) MF_CS(2, 6) MF_CS(3, 7)
+          }
+        } else {
+          const bool lower = (g.lane() & j) == 0;
+#pragma unroll
+          for (int m = 0; m < E; ++m) {
+            if (m < nm) {
+              const unsigned long long ph = g.shfl_xor(h[m], j);
+              const unsigned pl = (unsigned)g.shfl_xor((int)lo[m], j);
+              const bool up = ((m * G::N + g.lane()) & k) == 0;
+              const bool take = (lower == up) ? kv_gt(h[m], lo[m], ph, pl) : kv_gt(ph, pl, h[m], lo[m]);
+              if (take) {
+                h[m] = ph;
+                lo[m] = pl;
+              }
+            }
+          }
+        }
+      }
+    }
+#undef MF_CS
+    g.sync();
+#pragma unroll
+    for (int m = 0; m < E; ++m) {
+      const int i = m * G::N + g.lane();
+      if (m < nm && i < n) {
+        xh[i] = h[m];
+        xl[i] = lo[m];
+      }
+    }
+    g.sync();
+  }
+
+#endif
   template <bool kLinksOnChip>
   MF_NOINLINE void allocate_slots(int ncls, bool has_caps) {
     const int A = s.n_active;
@@ -1933,6 +1985,17 @@ MF_UNROLL
       }
       MF_TOC(OUT_CY_SUB + 1, q1);
       if (nt > s.max_touch) s.max_touch = nt;
+#if defined(MF_CAP_SORT)
+      // capped members sorted by cap once per class (rounds then walk a prefix)
+      const bool csorted = ncap > 1 && ncap <= kCapSort;
+      const int ctot = ncap;
+      int cpos = 0;
+      if (csorted) sort_caps(ncap);
+#else
+      constexpr bool csorted = false;
+      const int ctot = 0;
+      int cpos = 0;
+#endif
       int nu = n;
       double R = 0.0;
       while (nu > 0) {
@@ -2041,7 +2104,37 @@ MF_UNROLL
         // cap freezes (the same rate R, so the order against the link freezes
         // is immaterial): drop frozen entries, freeze cap - eps <= R, and take
         // the minimum cap of the survivors for the next round
-        if (ncap > 0) {
+        if (ncap > 0 && csorted) {
+          // cap-sorted entries: R >= cap - 1e-12 max(1, cap) holds on a prefix
+          // (the threshold is increasing in cap), so the pass is a pointer
+          // walk; entries frozen through a link are stepped over
+          for (;;) {
+            const int i = cpos + g.lane();
+            bool pass = false, fz = false;
+            int p = 0;
+            if (i < ctot) {
+              p = (int)I.x_lo[i];
+              const bool was = (frz[p >> 5] & (1u << (p & 31))) != 0u;
+              const double cp = bits_to_d(I.x_hi[i]);
+              fz = !was && R >= dsub(cp, dmul(1e-12, smax(1.0, cp)));
+              pass = was || fz;
+            }
+            const unsigned stop = g.ballot(!pass);
+            const int adv = stop ? ctz32(stop) : G::N;
+            if (fz && g.lane() < adv) {
+              g.atomic_or(&frz[p >> 5], 1u << (p & 31));
+              rate[p] = R;
+              const int rn = arnp[p];
+              route_slots_add(cnt, asl + p * RM, rn, -1);
+              ++got;
+            }
+            cpos = cpos + adv < ctot ? cpos + adv : ctot;
+            if (stop || cpos >= ctot) break;
+          }
+          g.sync();
+          ncap = ctot - cpos;
+          cmn = ncap > 0 ? bits_to_d(I.x_hi[cpos]) : MF_INF;
+        } else if (ncap > 0) {
           int nc2 = 0;
           double mn = MF_INF;
           for (int base = 0; base < ncap; base += G::N) {
