@@ -1457,6 +1457,10 @@ MF_UNROLL
   // active order (baselines.cpp:102-133), via stable bucketing by link.
   MF_NOINLINE void karuna_caps(int nd) {
     const int A = s.n_active;
+    // demand per link slot in the (usually on-chip) slot residual array, which
+    // is free until the filling; per link in HBM when some route has no slot
+    const bool slots = slot_mode();
+    double* __restrict__ dm = slots ? I.sl_res : I.l_x;
     for (int p = g.lane(); p < A; p += G::N) I.s_cap[p] = MF_INF;
     g.sync();
     // want = remaining / slack for positive slack; demand on the touched links zeroed
@@ -1466,7 +1470,7 @@ MF_UNROLL
       if (slack > 0.0) {
         I.s_cap[p] = ddiv(I.a_rem[p], slack);  // stash: capped below
         const int rn = arn(p);
-        for (int k = 0; k < rn; ++k) I.l_x[arl(p, k)] = 0.0;
+        for (int k = 0; k < rn; ++k) dm[entry_key(p, k)] = 0.0;
       }
     }
     g.sync();
@@ -1488,8 +1492,8 @@ MF_UNROLL
         const int pt = g.shfl(p, t);
         const double w = g.shfl(want, t);
         for (int k = g.lane(); k < rt; k += G::N) {
-          const int l = arl(pt, k);
-          I.l_x[l] = dadd(I.l_x[l], w);
+          const int e = entry_key(pt, k);
+          dm[e] = dadd(dm[e], w);
         }
         g.sync();
       }
@@ -1503,7 +1507,7 @@ MF_UNROLL
       for (int k = 0; k < rn; ++k) {
         const int l = arl(p, k);
         const double c = I.cap[l];
-        const double dmd = I.l_x[l];
+        const double dmd = dm[entry_key(p, k)];
         if (dmd > c) scale = smin(scale, ddiv(c, dmd));
       }
       I.s_cap[p] = dmul(want, scale);
@@ -1744,100 +1748,6 @@ MF_UNROLL
     for (int k = 0; k < rn; ++k) g.atomic_add(&cnt[sl[k]], v);
   }
 
-#if defined(MF_CAP_SORT)
-  // Ascending sort of the capped entries (x_hi = cap bits, x_lo = active
-  // position) of one class, n <= kCapSort: a bitonic network over registers
-  // (8 entries per lane; lane-crossing stages by shuffle, register-crossing
-  // stages by static pairs). Caps are >= 0, so their bit patterns order like
-  // the values; equal caps may come out in any order (they freeze together).
-  static constexpr int kCapSort = 8 * G::N;
-  MF_FN static bool kv_gt(unsigned long long ha, unsigned la, unsigned long long hb, unsigned lb) {
-    return ha > hb || (ha == hb && la > lb);
-  }
-  MF_NOINLINE void sort_caps(int n) {
-    unsigned long long* __restrict__ xh = I.x_hi;
-    unsigned long long* __restrict__ xl = I.x_lo;
-    if (G::N == 1) {  // serial build: insertion sort
-      for (int i = 1; i < n; ++i) {
-        const unsigned long long h = xh[i], l = xl[i];
-        int j = i - 1;
-        while (j >= 0 && kv_gt((unsigned long long)xh[j], (unsigned)xl[j], h, (unsigned)l)) {
-          xh[j + 1] = xh[j];
-          xl[j + 1] = xl[j];
-          --j;
-        }
-        xh[j + 1] = h;
-        xl[j + 1] = l;
-      }
-      return;
-    }
-    constexpr int E = 8;
-    int n2 = G::N;
-    while (n2 < n) n2 <<= 1;
-    const int nm = n2 / G::N;
-    unsigned long long h[E];
-    unsigned lo[E];
-#pragma unroll
-    for (int m = 0; m < E; ++m) {
-      const int i = m * G::N + g.lane();
-      h[m] = i < n ? xh[i] : ~0ull;
-      lo[m] = i < n ? (unsigned)xl[i] : ~0u;
-    }
-#define MF_CS(a, b)                                                   \
-  if ((b) < nm) {                                                      \
-    const bool up = (((a)*G::N + g.lane()) & k) == 0;                  \
-    if (kv_gt(h[a], lo[a], h[b], lo[b]) == up) {                       \
-      const unsigned long long th = h[a];                              \
-      const unsigned tl_ = lo[a];                                      \
-      h[a] = h[b];                                                     \
-      lo[a] = lo[b];                                                   \
-      h[b] = th;                                                       \
-      lo[b] = tl_;                                                     \
-    }                                                                  \
-  }
-    for (int k = 2; k <= n2; k <<= 1) {
-      for (int j = k >> 1; j > 0; j >>= 1) {
-        if (j >= G::N) {
-          const int jm = j / G::N;
-          if (jm == 1) {
-            MF_CS(0, 1) MF_CS(2, 3) MF_CS(4, 5) MF_CS(6, 7)
-          } else if (jm == 2) {
-            MF_CS(0, 2) MF_CS(1, 3) MF_CS(4, 6) MF_CS(5, 7)
-          } else {
-            MF_CS(0, 4) MF_CS(1, 5) MF_CS(2, 6) MF_CS(3, 7)
-          }
-        } else {
-          const bool lower = (g.lane() & j) == 0;
-#pragma unroll
-          for (int m = 0; m < E; ++m) {
-            if (m < nm) {
-              const unsigned long long ph = g.shfl_xor(h[m], j);
-              const unsigned pl = (unsigned)g.shfl_xor((int)lo[m], j);
-              const bool up = ((m * G::N + g.lane()) & k) == 0;
-              const bool take = (lower == up) ? kv_gt(h[m], lo[m], ph, pl) : kv_gt(ph, pl, h[m], lo[m]);
-              if (take) {
-                h[m] = ph;
-                lo[m] = pl;
-              }
-            }
-          }
-        }
-      }
-    }
-#undef MF_CS
-    g.sync();
-#pragma unroll
-    for (int m = 0; m < E; ++m) {
-      const int i = m * G::N + g.lane();
-      if (m < nm && i < n) {
-        xh[i] = h[m];
-        xl[i] = lo[m];
-      }
-    }
-    g.sync();
-  }
-
-#endif
   template <bool kLinksOnChip>
   MF_NOINLINE void allocate_slots(int ncls, bool has_caps) {
     const int A = s.n_active;
@@ -1985,17 +1895,6 @@ MF_UNROLL
       }
       MF_TOC(OUT_CY_SUB + 1, q1);
       if (nt > s.max_touch) s.max_touch = nt;
-#if defined(MF_CAP_SORT)
-      // capped members sorted by cap once per class (rounds then walk a prefix)
-      const bool csorted = ncap > 1 && ncap <= kCapSort;
-      const int ctot = ncap;
-      int cpos = 0;
-      if (csorted) sort_caps(ncap);
-#else
-      constexpr bool csorted = false;
-      const int ctot = 0;
-      int cpos = 0;
-#endif
       int nu = n;
       double R = 0.0;
       while (nu > 0) {
@@ -2104,37 +2003,7 @@ MF_UNROLL
         // cap freezes (the same rate R, so the order against the link freezes
         // is immaterial): drop frozen entries, freeze cap - eps <= R, and take
         // the minimum cap of the survivors for the next round
-        if (ncap > 0 && csorted) {
-          // cap-sorted entries: R >= cap - 1e-12 max(1, cap) holds on a prefix
-          // (the threshold is increasing in cap), so the pass is a pointer
-          // walk; entries frozen through a link are stepped over
-          for (;;) {
-            const int i = cpos + g.lane();
-            bool pass = false, fz = false;
-            int p = 0;
-            if (i < ctot) {
-              p = (int)I.x_lo[i];
-              const bool was = (frz[p >> 5] & (1u << (p & 31))) != 0u;
-              const double cp = bits_to_d(I.x_hi[i]);
-              fz = !was && R >= dsub(cp, dmul(1e-12, smax(1.0, cp)));
-              pass = was || fz;
-            }
-            const unsigned stop = g.ballot(!pass);
-            const int adv = stop ? ctz32(stop) : G::N;
-            if (fz && g.lane() < adv) {
-              g.atomic_or(&frz[p >> 5], 1u << (p & 31));
-              rate[p] = R;
-              const int rn = arnp[p];
-              route_slots_add(cnt, asl + p * RM, rn, -1);
-              ++got;
-            }
-            cpos = cpos + adv < ctot ? cpos + adv : ctot;
-            if (stop || cpos >= ctot) break;
-          }
-          g.sync();
-          ncap = ctot - cpos;
-          cmn = ncap > 0 ? bits_to_d(I.x_hi[cpos]) : MF_INF;
-        } else if (ncap > 0) {
+        if (ncap > 0) {
           int nc2 = 0;
           double mn = MF_INF;
           for (int base = 0; base < ncap; base += G::N) {
