@@ -1457,10 +1457,7 @@ MF_UNROLL
   // active order (baselines.cpp:102-133), via stable bucketing by link.
   MF_NOINLINE void karuna_caps(int nd) {
     const int A = s.n_active;
-    // demand per link slot in the (usually on-chip) slot residual array, which
-    // is free until the filling; per link in HBM when some route has no slot
-    const bool slots = slot_mode();
-    double* __restrict__ dm = slots ? I.sl_res : I.l_x;
+    double* __restrict__ dm = I.l_x;  // per-link demand
     for (int p = g.lane(); p < A; p += G::N) I.s_cap[p] = MF_INF;
     g.sync();
     // want = remaining / slack for positive slack; demand on the touched links zeroed
@@ -1470,7 +1467,7 @@ MF_UNROLL
       if (slack > 0.0) {
         I.s_cap[p] = ddiv(I.a_rem[p], slack);  // stash: capped below
         const int rn = arn(p);
-        for (int k = 0; k < rn; ++k) dm[entry_key(p, k)] = 0.0;
+        for (int k = 0; k < rn; ++k) dm[arl(p, k)] = 0.0;
       }
     }
     g.sync();
@@ -1492,8 +1489,8 @@ MF_UNROLL
         const int pt = g.shfl(p, t);
         const double w = g.shfl(want, t);
         for (int k = g.lane(); k < rt; k += G::N) {
-          const int e = entry_key(pt, k);
-          dm[e] = dadd(dm[e], w);
+          const int l = arl(pt, k);
+          dm[l] = dadd(dm[l], w);
         }
         g.sync();
       }
@@ -1507,7 +1504,7 @@ MF_UNROLL
       for (int k = 0; k < rn; ++k) {
         const int l = arl(p, k);
         const double c = I.cap[l];
-        const double dmd = dm[entry_key(p, k)];
+        const double dmd = dm[l];
         if (dmd > c) scale = smin(scale, ddiv(c, dmd));
       }
       I.s_cap[p] = dmul(want, scale);

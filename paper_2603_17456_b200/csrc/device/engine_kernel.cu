@@ -207,6 +207,14 @@ __global__ void __launch_bounds__(1024, 1)
   const int home = home_group(goff, n, groups, nsm, slice_ns);
   Engine<WarpLanes, kAalo> eng(*d, false);
   int state = 0;  // 0: claim next, 1: running an instance, 2: no work left
+  // first claims by block: the gang's warps take consecutive instances of the
+  // claim order (similar per-event cost, so less waiting at the barrier)
+  __shared__ int base0;
+  if (threadIdx.x == 0) base0 = atomicAdd(&next[home], nw);
+  __syncthreads();
+  int first = -1;
+  if (goff[home] + base0 + (int)(threadIdx.x >> 5) < goff[home + 1])
+    first = order[goff[home] + base0 + (threadIdx.x >> 5)];
 #if defined(MF_GANG_PROF)
   // lock-step efficiency: busy cycles of this warp's events vs the whole loop
   __shared__ unsigned long long busy_sum, iters;
@@ -217,7 +225,8 @@ __global__ void __launch_bounds__(1024, 1)
 #endif
   for (;;) {
     if (state == 0) {
-      const int i = claim(order, goff, groups, home, next);
+      const int i = first >= 0 ? first : claim(order, goff, groups, home, next);
+      first = -1;
       if (i < 0) {
         state = 2;
       } else {
@@ -349,16 +358,6 @@ class CudaBackend final : public Backend {
     // instances left, ceil(active / SMs) warps per SM keep them on distinct SMs
     const int want = (active + sms_ - 1) / sms_;
     if (want < per_sm) per_sm = want > 0 ? want : 1;
-    // A sparse launch (a few instances per SM: big single instances, the tail
-    // of a batch) needs little shared memory; the rest of the SM's 228 KB then
-    // serves as L1 for the instances' HBM-resident state (a lone warp is bound
-    // by load latency, L1 ~30 cycles vs L2 ~250)
-    const int carve = std::min(100, (per_sm * plan.bytes * 100 + 228 * 1024 - 1) / (228 * 1024) + 1);
-    const int ki = hint.aalo ? 1 : 0;
-    if (carve != carve_[ki]) {
-      ck(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, carve), "carveout");
-      carve_[ki] = carve;
-    }
     int grid = sms_ * per_sm;
     ck(cudaMemsetAsync(counter_ + 1, 0, sizeof(int) * kMaxGroups, stream_), "memset");
     ck(cudaEventRecord(e0_, stream_), "event");
@@ -430,7 +429,6 @@ class CudaBackend final : public Backend {
   int gang_ = 32;  // warps per block in lock step (MFSIM_GANG; 1 = one-warp kernel)
   const char* last_kernel_ = "";
   int gang_min_ = -1;  // fewest instances for a gang launch (-1: a full gang per SM)
-  int carve_[2] = {-1, -1};  // shared-memory carveout (%) last set on the one-warp kernels
   int fill_busy_ = 32;  // extra events while more than this many warps are busy (32: none)
   int last_grid_ = 0;
   int launches_ = 0;

@@ -986,13 +986,17 @@ void Batch::pack() {
   }
   for (int i = 0; i < n; ++i) desc_[i].phase = phase_dev_ + i;
   // claim order: estimated work descending (Karuna's capped filling and MFS's
-  // promotions cost the most per event), so the longest instances start first
+  // promotions cost the most per event; the per-event cost grows with the
+  // offered load, i.e. the active set), so the longest instances start first
+  // and consecutive claims -- the 32 warps of a lock-step gang -- get
+  // instances of similar per-event cost
   std::vector<double> cost(n);
   for (int i = 0; i < n; ++i) {
     const Inst& d = desc_[i];
     static const double factor[] = {1.0, 1.6, 1.1, 12.0, 2.5, 1.5, 4.0};
     const int pol = d.p.policy >= 0 && d.p.policy < 7 ? d.p.policy : 0;
-    cost[i] = factor[pol] * (double(d.F_cap) + 2.0 * d.n_req);
+    const double load = inputs_[i].rate > 0.0 ? inputs_[i].rate : 1.0;
+    cost[i] = factor[pol] * (double(d.F_cap) + 2.0 * d.n_req) * (1.0 + load);
   }
   // claim groups: one per policy, so that the warps sharing an SM run the same
   // policy's code (the engine's instruction footprint exceeds the i-cache)
@@ -1000,7 +1004,8 @@ void Batch::pack() {
   std::iota(order_.begin(), order_.end(), 0);
   std::stable_sort(order_.begin(), order_.end(), [&](int a, int b) {
     if (desc_[a].p.policy != desc_[b].p.policy) return desc_[a].p.policy < desc_[b].p.policy;
-    return cost[a] > cost[b];
+    if (cost[a] != cost[b]) return cost[a] > cost[b];
+    return inputs_[a].slo_mult > inputs_[b].slo_mult;
   });
   std::vector<int> off{0};
   for (int k = 1; k < n; ++k)
