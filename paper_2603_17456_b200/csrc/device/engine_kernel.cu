@@ -184,16 +184,10 @@ template <bool kAalo>
 __global__ void __launch_bounds__(1024, 1)
     mfsim_gang_kernel(const Inst* __restrict__ insts, const int* __restrict__ order, int n,
                       int groups, int nsm, int* __restrict__ next, SmemPlan plan,
-                      long long budget, long long slice_ns, int* __restrict__ remaining,
-                      int fill_busy) {
+                      long long budget, long long slice_ns, int* __restrict__ remaining) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ unsigned long long t0;
-  // warps whose first event of the current interval is done (by interval parity)
-  __shared__ int ndone[2];
-  if (threadIdx.x == 0) ndone[0] = ndone[1] = 0;
-  __syncthreads();
   const int nw = blockDim.x >> 5;
-  int par = 0;
   const int lane = threadIdx.x & 31;
   unsigned char* mine = smem + (threadIdx.x >> 5) * plan.bytes;
   Inst* d = reinterpret_cast<Inst*>(mine);
@@ -238,13 +232,7 @@ __global__ void __launch_bounds__(1024, 1)
 #if defined(MF_GANG_PROF)
       const long long b0 = clock64();
 #endif
-      int r = eng.step(deadline);
-      if (fill_busy < nw) {
-        // while many warps of the gang are still in their event, more events
-        // of this instance cost no barrier time
-        if (lane == 0) atomicAdd(&ndone[par], 1);
-        while (r == 0 && nw - *(volatile int*)&ndone[par] > fill_busy) r = eng.step(deadline);
-      }
+      const int r = eng.step(deadline);
 #if defined(MF_GANG_PROF)
       busy += clock64() - b0;
       ++n_it;
@@ -256,10 +244,7 @@ __global__ void __launch_bounds__(1024, 1)
         state = 0;
       }
     }
-    if (fill_busy < nw && state != 1 && lane == 0) atomicAdd(&ndone[par], 1);
     if (!__syncthreads_or(state != 2)) break;
-    if (threadIdx.x == 0) ndone[par ^ 1] = 0;  // last used two intervals ago
-    par ^= 1;
   }
 #if defined(MF_GANG_PROF)
   if (lane == 0) {
@@ -307,7 +292,6 @@ class CudaBackend final : public Backend {
     if (gang_ < 1) gang_ = 1;
     if (gang_ > 32) gang_ = 32;
     if (const char* g = getenv("MFSIM_GANG_MIN")) gang_min_ = atoi(g);  // tests: force small batches
-    if (const char* g = getenv("MFSIM_GANG_FILL")) fill_busy_ = atoi(g);
     // deep per-warp call chains (noinline handlers) need more than the default
     ck(cudaDeviceSetLimit(cudaLimitStackSize, 4096), "stack limit");
   }
@@ -385,7 +369,7 @@ class CudaBackend final : public Backend {
     ck(cudaEventRecord(e0_, stream_), "event");
     last_kernel_ = "mfsim_gang_kernel";
     kern<<<grid, threads, bytes, stream_>>>(d, order, n, hint.groups, sms_, counter_ + 1, plan,
-                                             budget, slice_ns, counter_, fill_busy_);
+                                             budget, slice_ns, counter_);
     ck(cudaGetLastError(), "launch");
     ck(cudaEventRecord(e1_, stream_), "event");
     ++launches_;
@@ -429,7 +413,6 @@ class CudaBackend final : public Backend {
   int gang_ = 32;  // warps per block in lock step (MFSIM_GANG; 1 = one-warp kernel)
   const char* last_kernel_ = "";
   int gang_min_ = -1;  // fewest instances for a gang launch (-1: a full gang per SM)
-  int fill_busy_ = 32;  // extra events while more than this many warps are busy (32: none)
   int last_grid_ = 0;
   int launches_ = 0;
   bool timed_ = false;

@@ -2,10 +2,8 @@
 workload, plus a bit-exactness check of every golden fixture under each gang size.
 
   python tools/gang_ab.py N SLICE_MS K SPEC1 SPEC2 ...
-SPEC = W[:noparity][:lib=PATH][:fill=K] (W = 1: the one-warp kernel; noparity:
-skip the fixture check; lib: an A/B build of the library instead of the
-product; fill: warps keep taking events while more than K warps of the gang
-are still in their first event of the interval).
+SPEC = W[:noparity][:lib=PATH] (W = 1: the one-warp kernel; noparity: skip the
+fixture check; lib: an A/B build of the library instead of the product).
 """
 import os
 import sys
@@ -31,10 +29,6 @@ for spec in sys.argv[4:]:
     w = int(parts[0])
     os.environ["MFSIM_GANG"] = str(w)
     os.environ["MFSIM_GANG_MIN"] = "1"
-    os.environ.pop("MFSIM_GANG_FILL", None)
-    for p in parts[1:]:
-        if p.startswith("fill="):
-            os.environ["MFSIM_GANG_FILL"] = p[5:]
     w = spec
     if "noparity" in parts:
         man, wl = [], []
