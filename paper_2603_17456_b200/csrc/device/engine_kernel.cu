@@ -327,9 +327,15 @@ class CudaBackend final : public Backend {
     // lock step pays off only when every SM holds a full gang: a batch of a
     // few (large) instances keeps one warp per instance, spread over the SMs
     if (active <= 0 || active > n) active = n;
-    if (gang_ > 1 && active >= (gang_min_ >= 0 ? gang_min_ : sms_ * gang_)) {
-      launch_gang(d, order, n, hint, budget, slice_ns, plan);
-      return;
+    if (gang_ > 1) {
+      // one gang block per SM of as many warps as the running instances fill
+      // (up to MFSIM_GANG); thinner than kMinGang warps the one-warp kernel is used
+      const bool forced = gang_min_ >= 0 && active >= gang_min_;
+      const int w = forced ? gang_ : std::min(gang_, active / sms_);
+      if (forced || w >= kMinGang) {
+        launch_gang(d, order, n, hint, budget, slice_ns, plan, w);
+        return;
+      }
     }
     int per_sm = 0;
     // the lean kernel unless the batch holds Aalo instances (extension code compiled out)
@@ -355,15 +361,15 @@ class CudaBackend final : public Backend {
     last_grid_ = grid;
   }
   void launch_gang(const mfb::Inst* d, const int* order, int n, const LaunchHint& hint,
-                   long long budget, long long slice_ns, const mfb::SmemPlan& plan) {
+                   long long budget, long long slice_ns, const mfb::SmemPlan& plan, int w) {
     auto kern = hint.aalo ? mfb::mfsim_gang_kernel<true> : mfb::mfsim_gang_kernel<false>;
-    const int threads = 32 * gang_;
-    const int bytes = plan.bytes * gang_;
+    const int threads = 32 * w;
+    const int bytes = plan.bytes * w;
     int per_sm = 0;
     ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, bytes), "occupancy");
     if (per_sm < 1) throw DeviceError("gang block does not fit an SM");
-    int grid = sms_ * per_sm;
-    const int need = (n + gang_ - 1) / gang_;
+    int grid = sms_;  // one gang per SM: its warps share the SM's instruction cache
+    const int need = (n + w - 1) / w;
     if (need < grid) grid = need > 0 ? need : 1;
     ck(cudaMemsetAsync(counter_ + 1, 0, sizeof(int) * kMaxGroups, stream_), "memset");
     ck(cudaEventRecord(e0_, stream_), "event");
@@ -411,6 +417,7 @@ class CudaBackend final : public Backend {
   int* remain_host_ = nullptr;
   int sms_ = 148;
   int gang_ = 32;  // warps per block in lock step (MFSIM_GANG; 1 = one-warp kernel)
+  static constexpr int kMinGang = 16;  // thinnest gang worth its barrier
   const char* last_kernel_ = "";
   int gang_min_ = -1;  // fewest instances for a gang launch (-1: a full gang per SM)
   int last_grid_ = 0;

@@ -2,8 +2,10 @@
 workload, plus a bit-exactness check of every golden fixture under each gang size.
 
   python tools/gang_ab.py N SLICE_MS K SPEC1 SPEC2 ...
-SPEC = W[:noparity][:lib=PATH] (W = 1: the one-warp kernel; noparity: skip the
-fixture check; lib: an A/B build of the library instead of the product).
+SPEC = W[:noparity][:lib=PATH][:nomin] (W = 1: the one-warp kernel; noparity:
+skip the fixture check; lib: an A/B build of the library instead of the
+product; nomin: no forced gang for small batches -- the library sizes the gang
+to the running instances itself).
 """
 import os
 import sys
@@ -29,6 +31,8 @@ for spec in sys.argv[4:]:
     w = int(parts[0])
     os.environ["MFSIM_GANG"] = str(w)
     os.environ["MFSIM_GANG_MIN"] = "1"
+    if "nomin" in parts:  # the library's own choice of kernel and gang size
+        os.environ.pop("MFSIM_GANG_MIN")
     w = spec
     if "noparity" in parts:
         man, wl = [], []
