@@ -1892,31 +1892,6 @@ MF_UNROLL
       }
       MF_TOC(OUT_CY_SUB + 1, q1);
       if (nt > s.max_touch) s.max_touch = nt;
-#if defined(MF_LANE_CAPS)
-      // Capped members as per-lane sorted lists: lane L owns entries L, L+N,
-      // L+2N, ... and sorts them by cap (insertion sort, serial per lane);
-      // R >= cap - eps holds on a prefix of every list (the threshold grows
-      // with the cap), so a round only looks at each lane's head.
-      const int kl = ncap > g.lane() ? (ncap - g.lane() + G::N - 1) / G::N : 0;
-      int hd = 0;
-      {
-        unsigned long long* __restrict__ xh = I.x_hi;
-        unsigned long long* __restrict__ xl = I.x_lo;
-        const int L = g.lane();
-        for (int a = 1; a < kl; ++a) {
-          const unsigned long long h = xh[L + a * G::N], lo = xl[L + a * G::N];
-          int b = a - 1;
-          while (b >= 0 && xh[L + b * G::N] > h) {
-            xh[L + (b + 1) * G::N] = xh[L + b * G::N];
-            xl[L + (b + 1) * G::N] = xl[L + b * G::N];
-            --b;
-          }
-          xh[L + (b + 1) * G::N] = h;
-          xl[L + (b + 1) * G::N] = lo;
-        }
-        g.sync();
-      }
-#endif
       int nu = n;
       double R = 0.0;
       while (nu > 0) {
@@ -2025,36 +2000,6 @@ MF_UNROLL
         // cap freezes (the same rate R, so the order against the link freezes
         // is immaterial): drop frozen entries, freeze cap - eps <= R, and take
         // the minimum cap of the survivors for the next round
-#if defined(MF_LANE_CAPS)
-        if (ncap > 0) {
-          // each lane pops its head: entries frozen through a link, then cap
-          // freezes; its next live entry is the lane's smallest live cap
-          double lc = MF_INF;
-          while (hd < kl) {
-            const int e = g.lane() + hd * G::N;
-            const int p = (int)I.x_lo[e];
-            const unsigned bit = 1u << (p & 31);
-            if (frz[p >> 5] & bit) {
-              ++hd;
-              continue;
-            }
-            const double cp = bits_to_d(I.x_hi[e]);
-            if (R >= dsub(cp, dmul(1e-12, smax(1.0, cp)))) {
-              g.atomic_or(&frz[p >> 5], bit);
-              rate[p] = R;
-              route_slots_add(cnt, asl + p * RM, arnp[p], -1);
-              ++got;
-              ++hd;
-              continue;
-            }
-            lc = cp;
-            break;
-          }
-          cmn = g.min_nonneg(lc);  // stored caps are smax(0, cap) >= 0
-          ncap = g.any(hd < kl) ? 1 : 0;  // some live capped member is left
-          g.sync();
-        }
-#else
         if (ncap > 0) {
           int nc2 = 0;
           double mn = MF_INF;
@@ -2093,7 +2038,6 @@ MF_UNROLL
           ncap = nc2;
           cmn = mn;
         }
-#endif
         int frozen = 0;
         if (ns > 0 || has_caps) {
           int tot;
