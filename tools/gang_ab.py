@@ -33,6 +33,10 @@ for spec in sys.argv[4:]:
     os.environ["MFSIM_GANG_MIN"] = "1"
     if "nomin" in parts:  # the library's own choice of kernel and gang size
         os.environ.pop("MFSIM_GANG_MIN")
+    for p in parts[1:]:  # MFSIM_*=value: an environment knob for this spec only
+        if p.startswith("MFSIM_") and "=" in p:
+            k, v = p.split("=", 1)
+            os.environ[k] = v
     w = spec
     if "noparity" in parts:
         man, wl = [], []
@@ -81,3 +85,6 @@ for spec in sys.argv[4:]:
     print(f"gang {w} n={n}: {(e1 - e0) / ms * 1e3 / 1e6:.3f} M events/s "
           f"({e1 - e0} events in {ms:.0f} ms, setup {setup:.1f}s)", flush=True)
     del b
+    for p in parts[1:]:
+        if p.startswith("MFSIM_") and "=" in p:
+            os.environ.pop(p.split("=", 1)[0], None)
