@@ -303,12 +303,14 @@ def main():
     ev0, by0 = progress()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
+    launches0 = batch.kernel_launches
     with Clocks(local) as clk:
         start.record(stream)
         for _ in range(args.steps):
             batch.launch_slice(int(args.slice_ms * 1e6))
         end.record(stream)
         barrier()
+    launches = batch.kernel_launches - launches0
     dev_ms = start.elapsed_time(end)
     ev1, by1 = progress()
     events, algo_bytes = ev1 - ev0, by1 - by0
@@ -354,7 +356,7 @@ def main():
             "config": workload_config(args),
             "e2e": {"value": e2e, "unit": "events/s", "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h)},
-            "gpu_launches": args.steps,
+            "gpu_launches": launches,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                          "kernel": batch.last_kernel,

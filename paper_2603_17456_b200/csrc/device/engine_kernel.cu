@@ -176,7 +176,10 @@ class CudaBackend final : public Backend {
         ck(cudaMalloc(&order_tmp_, need * sizeof(int)), "cudaMalloc order");
         order_tmp_cap_ = need;
       }
-      if (mfb::order_kernel_launch(stream_, d, order, order_tmp_, n, hint.groups)) ord = order_tmp_;
+      if (mfb::order_kernel_launch(stream_, d, order, order_tmp_, n, hint.groups)) {
+        ord = order_tmp_;
+        ++launches_;
+      }
     }
     last_kernel_ = "mfsim_gang_kernel";
     mfb::gang_kernel_launch(hint.aalo, grid, threads, bytes, stream_, d, ord, n, hint.groups, sms_, counter_ + 1,
