@@ -35,8 +35,8 @@ for spec in sys.argv[4:]:
         os.environ.pop("MFSIM_GANG_MIN")
     for p in parts[1:]:  # MFSIM_*=value: an environment knob for this spec only
         if p.startswith("MFSIM_") and "=" in p:
-            k, v = p.split("=", 1)
-            os.environ[k] = v
+            knob, val = p.split("=", 1)
+            os.environ[knob] = val
     w = spec
     if "noparity" in parts:
         man, wl = [], []
