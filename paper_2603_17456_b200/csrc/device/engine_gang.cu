@@ -91,64 +91,6 @@ __global__ void __launch_bounds__(1024, 1)
 #endif
 }
 
-// Re-sorts every claim group by its instances' CURRENT active-flow count,
-// descending, before a time-sliced gang launch: the 32 warps of a gang then
-// take instances of similar per-event cost at this point of their runs (the
-// static claim order only knows the offered load). A suspended instance's
-// count is in its scalar-state blob; fresh and finished instances count 0.
-// One block; keys (group, -active, position) bitonic-sorted in shared memory.
-__global__ void __launch_bounds__(1024)
-    mfsim_order_kernel(const Inst* __restrict__ insts, const int* __restrict__ in, int* __restrict__ out,
-                       int n, int groups, int n2) {
-  extern __shared__ __align__(16) unsigned long long key[];
-  const int* __restrict__ goff = in + n;
-  for (int i = threadIdx.x; i < n2; i += blockDim.x) {
-    unsigned long long k = ~0ull;
-    if (i < n) {
-      const int id = in[i];
-      int g = 0;
-      while (g + 1 < groups && goff[g + 1] <= i) ++g;
-      int a = 0;
-      if (*insts[id].phase == 1) a = reinterpret_cast<const Sc*>(insts[id].sc_blob)->n_active;
-      a = a < 0 ? 0 : (a > 0xFFFFF ? 0xFFFFF : a);
-      k = ((unsigned long long)g << 52) | ((unsigned long long)(0xFFFFF - a) << 32) | (unsigned)i;
-    }
-    key[i] = k;
-  }
-  __syncthreads();
-  for (int k = 2; k <= n2; k <<= 1) {
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int i = threadIdx.x; i < n2; i += blockDim.x) {
-        const int ixj = i ^ j;
-        if (ixj > i) {
-          const unsigned long long a = key[i], b = key[ixj];
-          if (((i & k) == 0) == (a > b)) {
-            key[i] = b;
-            key[ixj] = a;
-          }
-        }
-      }
-      __syncthreads();
-    }
-  }
-  for (int i = threadIdx.x; i < n; i += blockDim.x) out[i] = in[(int)(key[i] & 0xffffffffu)];
-  for (int i = threadIdx.x; i < 2 * (groups + 1); i += blockDim.x) out[n + i] = in[n + i];
-}
-
-bool order_kernel_launch(cudaStream_t stream, const Inst* insts, const int* in, int* out, int n, int groups) {
-  int n2 = 1;
-  while (n2 < n) n2 <<= 1;
-  const int bytes = n2 * 8;
-  if (bytes > 200 * 1024) return false;
-  static bool init = false;
-  if (!init) {
-    cudaFuncSetAttribute(mfsim_order_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    init = true;
-  }
-  mfsim_order_kernel<<<1, 1024, bytes, stream>>>(insts, in, out, n, groups, n2);
-  return true;
-}
-
 void gang_kernel_init() {
   for (auto k : {mfsim_gang_kernel<false>, mfsim_gang_kernel<true>})
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);

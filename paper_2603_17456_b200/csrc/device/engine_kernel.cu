@@ -86,12 +86,10 @@ class CudaBackend final : public Backend {
     if (gang_ < 1) gang_ = 1;
     if (gang_ > 32) gang_ = 32;
     if (const char* g = getenv("MFSIM_GANG_MIN")) gang_min_ = atoi(g);  // tests: force small batches
-    if (const char* g = getenv("MFSIM_GANG_RESORT")) resort_ = atoi(g) != 0;
     // deep per-warp call chains (noinline handlers) need more than the default
     ck(cudaDeviceSetLimit(cudaLimitStackSize, 4096), "stack limit");
   }
   ~CudaBackend() override {
-    if (order_tmp_) cudaFree(order_tmp_);
     cudaFree(counter_);
     cudaFreeHost(remain_host_);
     cudaEventDestroy(e0_);
@@ -167,20 +165,7 @@ class CudaBackend final : public Backend {
     if (need < grid) grid = need > 0 ? need : 1;
     ck(cudaMemsetAsync(counter_ + 1, 0, sizeof(int) * kMaxGroups, stream_), "memset");
     ck(cudaEventRecord(e0_, stream_), "event");
-    // time slices: the gang's claim order follows the instances' current active sets
     const int* ord = order;
-    if (resort_ && slice_ns > 0) {
-      const size_t need = static_cast<size_t>(n) + 2 * (kMaxGroups + 1);
-      if (need > order_tmp_cap_) {
-        if (order_tmp_) cudaFree(order_tmp_);
-        ck(cudaMalloc(&order_tmp_, need * sizeof(int)), "cudaMalloc order");
-        order_tmp_cap_ = need;
-      }
-      if (mfb::order_kernel_launch(stream_, d, order, order_tmp_, n, hint.groups)) {
-        ord = order_tmp_;
-        ++launches_;
-      }
-    }
     last_kernel_ = "mfsim_gang_kernel";
     mfb::gang_kernel_launch(hint.aalo, grid, threads, bytes, stream_, d, ord, n, hint.groups, sms_, counter_ + 1,
                             plan, budget, slice_ns, counter_);
@@ -227,9 +212,6 @@ class CudaBackend final : public Backend {
   int gang_ = 32;  // warps per block in lock step (MFSIM_GANG; 1 = one-warp kernel)
   static constexpr int kMinGang = 16;  // thinnest gang worth its barrier
   const char* last_kernel_ = "";
-  bool resort_ = true;  // time-sliced gangs claim by current active-set size (MFSIM_GANG_RESORT)
-  int* order_tmp_ = nullptr;
-  size_t order_tmp_cap_ = 0;
   int gang_min_ = -1;  // fewest instances for a gang launch (-1: a full gang per SM)
   int last_grid_ = 0;
   int launches_ = 0;

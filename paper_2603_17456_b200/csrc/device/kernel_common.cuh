@@ -134,8 +134,6 @@ static __device__ __forceinline__ int claim(const int* __restrict__ order, const
 // host side of the gang kernel (engine_gang.cu)
 void gang_kernel_init();
 int gang_kernel_blocks_per_sm(bool ext, int threads, int bytes);
-// the claim order re-sorted by current active-flow counts (false: batch too large)
-bool order_kernel_launch(cudaStream_t stream, const Inst* insts, const int* in, int* out, int n, int groups);
 void gang_kernel_launch(bool ext, int grid, int threads, int bytes, cudaStream_t stream, const Inst* insts,
                         const int* order, int n, int groups, int nsm, int* next, SmemPlan plan,
                         long long budget, long long slice_ns, int* remaining);
