@@ -1067,21 +1067,11 @@ void Batch::download(int detail) {
   // one D2H for every level-0 output of the batch (out[], ttft, stall, flags)
   be_.d2h(out_host_, out_dev_, out_bytes_);
   be_.sync();
-  for (int i = 0; i < size(); ++i) {
-    const Inst& d = desc_[i];
-    InstanceOutput& o = outputs_[i];
-    const OutView& ov = oview_[i];
-    std::memcpy(o.out, out_host_ + ov.out, sizeof(o.out));
-    const int n = d.n_req;
-    const double* tt = reinterpret_cast<const double*>(out_host_ + ov.ttft);
-    const double* st = reinterpret_cast<const double*>(out_host_ + ov.stall);
-    const uint8_t* pr = reinterpret_cast<const uint8_t*>(out_host_ + ov.pruned);
-    const int* rb = reinterpret_cast<const int*>(out_host_ + ov.rbatch);
-    o.ttft.assign(tt, tt + n);
-    o.stall.assign(st, st + n);
-    o.pruned.assign(pr, pr + n);
-    o.rbatch.assign(rb, rb + n);
-  }
+  // counters now; the per-request columns stay in the pinned buffer until an
+  // instance's output is read (output()), so a batch-wide read costs one copy
+  parsed_.assign(size(), 0);
+  for (int i = 0; i < size(); ++i)
+    std::memcpy(outputs_[i].out, out_host_ + oview_[i].out, sizeof(outputs_[i].out));
   if (detail >= 1) {
     for (int i = 0; i < size(); ++i) {
       const Inst& d = desc_[i];
@@ -1112,6 +1102,24 @@ void Batch::download(int detail) {
     }
     be_.sync();
   }
+}
+
+const InstanceOutput& Batch::output(int i) const {
+  InstanceOutput& o = outputs_[i];
+  if (i < static_cast<int>(parsed_.size()) && !parsed_[i]) {
+    const OutView& ov = oview_[i];
+    const int n = desc_[i].n_req;
+    const double* tt = reinterpret_cast<const double*>(out_host_ + ov.ttft);
+    const double* st = reinterpret_cast<const double*>(out_host_ + ov.stall);
+    const uint8_t* pr = reinterpret_cast<const uint8_t*>(out_host_ + ov.pruned);
+    const int* rb = reinterpret_cast<const int*>(out_host_ + ov.rbatch);
+    o.ttft.assign(tt, tt + n);
+    o.stall.assign(st, st + n);
+    o.pruned.assign(pr, pr + n);
+    o.rbatch.assign(rb, rb + n);
+    parsed_[i] = 1;
+  }
+  return o;
 }
 
 void Batch::run(int detail) {

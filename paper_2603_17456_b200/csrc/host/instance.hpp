@@ -145,7 +145,7 @@ class Batch {
 
   int size() const { return static_cast<int>(inputs_.size()); }
   const InstanceInput& input(int i) const { return inputs_[i]; }
-  const InstanceOutput& output(int i) const { return outputs_[i]; }
+  const InstanceOutput& output(int i) const;  // per-request columns parsed on first read
   size_t input_bytes() const { return in_bytes_; }
   size_t output_bytes(int detail) const;
   size_t device_bytes() const { return in_bytes_ + st_bytes_ + out_bytes_; }
@@ -155,7 +155,8 @@ class Batch {
   void release();
   Backend& be_;
   std::vector<InstanceInput> inputs_;
-  std::vector<InstanceOutput> outputs_;
+  mutable std::vector<InstanceOutput> outputs_;
+  mutable std::vector<char> parsed_;  // per-request columns copied out of out_host_
   std::vector<mfb::Inst> desc_;
   char* in_host_ = nullptr;
   char* out_host_ = nullptr;
