@@ -86,6 +86,7 @@ class CudaBackend final : public Backend {
     if (gang_ < 1) gang_ = 1;
     if (gang_ > 32) gang_ = 32;
     if (const char* g = getenv("MFSIM_GANG_MIN")) gang_min_ = atoi(g);  // tests: force small batches
+    if (const char* g = getenv("MFSIM_GANG_MINW")) min_gang_ = std::max(2, atoi(g));
     // deep per-warp call chains (noinline handlers) need more than the default
     ck(cudaDeviceSetLimit(cudaLimitStackSize, 4096), "stack limit");
   }
@@ -126,7 +127,7 @@ class CudaBackend final : public Backend {
       // (up to MFSIM_GANG); thinner than kMinGang warps the one-warp kernel is used
       const bool forced = gang_min_ >= 0 && active >= gang_min_;
       const int w = forced ? gang_ : std::min(gang_, active / sms_);
-      if (forced || w >= kMinGang) {
+      if (forced || w >= min_gang_) {
         launch_gang(d, order, n, hint, budget, slice_ns, plan, w);
         return;
       }
@@ -210,7 +211,7 @@ class CudaBackend final : public Backend {
   int* remain_host_ = nullptr;
   int sms_ = 148;
   int gang_ = 32;  // warps per block in lock step (MFSIM_GANG; 1 = one-warp kernel)
-  static constexpr int kMinGang = 16;  // thinnest gang worth its barrier
+  int min_gang_ = 16;  // thinnest gang worth its barrier (MFSIM_GANG_MINW)
   const char* last_kernel_ = "";
   int gang_min_ = -1;  // fewest instances for a gang launch (-1: a full gang per SM)
   int last_grid_ = 0;
