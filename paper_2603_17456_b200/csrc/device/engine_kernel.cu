@@ -211,7 +211,7 @@ class CudaBackend final : public Backend {
   int* remain_host_ = nullptr;
   int sms_ = 148;
   int gang_ = 32;  // warps per block in lock step (MFSIM_GANG; 1 = one-warp kernel)
-  int min_gang_ = 16;  // thinnest gang worth its barrier (MFSIM_GANG_MINW)
+  int min_gang_ = 12;  // thinnest gang worth its barrier (MFSIM_GANG_MINW; A/B: 13 warps +13 %, 9 warps +1 %)
   const char* last_kernel_ = "";
   int gang_min_ = -1;  // fewest instances for a gang launch (-1: a full gang per SM)
   int last_grid_ = 0;
