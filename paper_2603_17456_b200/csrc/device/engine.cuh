@@ -151,6 +151,8 @@ struct Sc {
   unsigned long long seq;
   long long events, steps, streak, pushes, algo_bytes, classes, rounds;
   long long stop_at;  // event count at which this launch suspends
+  int pend_ncls;      // classes of a rate recomputation split over gang barriers (-1: none)
+  bool pend_caps;
   int n_flows, n_batches, n_coflows, n_active, n_ev;
   int rp_top, pp_top, cm_top;
   int next_arr;
@@ -2074,6 +2076,39 @@ MF_UNROLL
     allocate(ncls, has_caps);
     MF_TOC(OUT_CY_ALLOC, t1);
     if (s.err) return;
+    resched();
+  }
+
+  // The rate recomputation in three parts for a lock-step gang (a barrier
+  // between each): the policy classes, the filling, the completion events.
+  MF_NOINLINE void settle_decide() {
+    s.pend_ncls = -1;
+    if (!s.dirty || s.err) return;
+    bool has_caps = false;
+    MF_TIC(t0);
+    const int ncls = decide(&has_caps);
+    MF_TOC(OUT_CY_DECIDE, t0);
+    if (s.err) return;
+    ++s.steps;
+    s.pend_ncls = ncls;
+    s.pend_caps = has_caps;
+  }
+  MF_NOINLINE void settle_allocate() {
+    if (s.pend_ncls < 0) return;
+    MF_TIC(t1);
+    allocate(s.pend_ncls, s.pend_caps);
+    MF_TOC(OUT_CY_ALLOC, t1);
+  }
+  MF_NOINLINE void settle_finish() {
+    if (s.pend_ncls < 0) return;
+    if (!s.err) resched();
+    s.dirty = 0;
+    s.pend_ncls = -1;
+  }
+
+  // changed rates -> new completion events, pushed in active_ order
+  // (engine.cpp:281-291)
+  MF_NOINLINE void resched() {
     MF_TIC(t2);
     const int A = s.n_active;
     const unsigned long long seq0 = s.seq;

@@ -8,10 +8,13 @@ namespace mfb {
 
 // Gang variant: a block of W warps, each owning its own instance (and its own
 // slice of shared memory), advances all W instances ONE EVENT at a time in
-// lock step (one block barrier per event). The engine is instruction-fetch
-// bound (ncu: 50-68 % of warp stalls "no instruction", ~40k SASS instructions,
-// warps of one SM in different phases); in lock step the W warps of a block
-// run through the same code at about the same time.
+// lock step, with a block barrier between the event, its policy classes, its
+// filling and its completion events. The engine is instruction-fetch bound
+// (ncu: 50-68 % of warp stalls "no instruction", ~40k SASS instructions, warps
+// of one SM in different phases); in lock step the W warps of a block run
+// through the same code at about the same time (A/B, profiles/r02_gang_ab.txt:
+// one barrier per event +13-15 %, the three phase barriers another +2.5 %,
+// two events per barrier -17 %).
 template <bool kAalo>
 __global__ void __launch_bounds__(1024, 1)
     mfsim_gang_kernel(const Inst* __restrict__ insts, const int* __restrict__ order, int n,
@@ -64,13 +67,41 @@ __global__ void __launch_bounds__(1024, 1)
 #if defined(MF_GANG_PROF)
       const long long b0 = clock64();
 #endif
-      const int r = eng.step(deadline);
+      const int r = eng.step_event(deadline);
 #if defined(MF_GANG_PROF)
       busy += clock64() - b0;
       ++n_it;
 #endif
       if (r != 0) {
         const bool done = eng.end(r == 1);
+        if (done && lane == 0) atomicSub(remaining, 1);
+        __syncwarp();
+        state = 0;
+      }
+    }
+    // barriers between the event, the policy classes, the filling and the
+    // completion events: the gang's warps run each phase's code together
+    __syncthreads();
+#if defined(MF_GANG_PROF)
+    long long b1 = clock64();
+#endif
+    if (state == 1) eng.settle_decide();
+#if defined(MF_GANG_PROF)
+    busy += clock64() - b1;
+#endif
+    __syncthreads();
+#if defined(MF_GANG_PROF)
+    b1 = clock64();
+#endif
+    if (state == 1) eng.settle_allocate();
+#if defined(MF_GANG_PROF)
+    busy += clock64() - b1;
+#endif
+    __syncthreads();
+    if (state == 1) {
+      eng.settle_finish();
+      if (eng.s.err) {
+        const bool done = eng.end(true);
         if (done && lane == 0) atomicSub(remaining, 1);
         __syncwarp();
         state = 0;
