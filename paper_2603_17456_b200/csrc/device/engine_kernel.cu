@@ -87,6 +87,7 @@ class CudaBackend final : public Backend {
     if (gang_ > 32) gang_ = 32;
     if (const char* g = getenv("MFSIM_GANG_MIN")) gang_min_ = atoi(g);  // tests: force small batches
     if (const char* g = getenv("MFSIM_GANG_MINW")) min_gang_ = std::max(2, atoi(g));
+    if (const char* g = getenv("MFSIM_GANG_BLOCKS")) gang_blocks_ = std::max(1, atoi(g));  // A/B only
     // deep per-warp call chains (noinline handlers) need more than the default
     ck(cudaDeviceSetLimit(cudaLimitStackSize, 4096), "stack limit");
   }
@@ -126,7 +127,7 @@ class CudaBackend final : public Backend {
       // one gang block per SM of as many warps as the running instances fill
       // (up to MFSIM_GANG); thinner than kMinGang warps the one-warp kernel is used
       const bool forced = gang_min_ >= 0 && active >= gang_min_;
-      const int w = forced ? gang_ : std::min(gang_, active / sms_);
+      const int w = forced ? gang_ : std::min(gang_, active / (sms_ * gang_blocks_));
       if (forced || w >= min_gang_) {
         launch_gang(d, order, n, hint, budget, slice_ns, plan, w);
         return;
@@ -161,7 +162,7 @@ class CudaBackend final : public Backend {
     const int bytes = plan.bytes * w;
     const int per_sm = mfb::gang_kernel_blocks_per_sm(hint.aalo, threads, bytes);
     if (per_sm < 1) throw DeviceError("gang block does not fit an SM");
-    int grid = sms_;  // one gang per SM: its warps share the SM's instruction cache
+    int grid = sms_ * std::min(gang_blocks_, per_sm);  // one gang per SM: its warps share the SM's instruction cache
     const int need = (n + w - 1) / w;
     if (need < grid) grid = need > 0 ? need : 1;
     ck(cudaMemsetAsync(counter_ + 1, 0, sizeof(int) * kMaxGroups, stream_), "memset");
@@ -211,6 +212,7 @@ class CudaBackend final : public Backend {
   int* remain_host_ = nullptr;
   int sms_ = 148;
   int gang_ = 32;  // warps per block in lock step (MFSIM_GANG; 1 = one-warp kernel)
+  int gang_blocks_ = 1;  // gang blocks per SM (MFSIM_GANG_BLOCKS, A/B)
   int min_gang_ = 12;  // thinnest gang worth its barrier (MFSIM_GANG_MINW; A/B: 13 warps +13 %, 9 warps +1 %)
   const char* last_kernel_ = "";
   int gang_min_ = -1;  // fewest instances for a gang launch (-1: a full gang per SM)
