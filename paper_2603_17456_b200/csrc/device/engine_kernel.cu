@@ -87,7 +87,7 @@ class CudaBackend final : public Backend {
     if (gang_ > 32) gang_ = 32;
     if (const char* g = getenv("MFSIM_GANG_MIN")) gang_min_ = atoi(g);  // tests: force small batches
     if (const char* g = getenv("MFSIM_GANG_MINW")) min_gang_ = std::max(2, atoi(g));
-    if (const char* g = getenv("MFSIM_GANG_BLOCKS")) gang_blocks_ = std::max(1, atoi(g));  // A/B only
+    if (const char* g = getenv("MFSIM_GANG_BLOCKS")) gang_blocks_ = std::max(1, atoi(g));
     // deep per-warp call chains (noinline handlers) need more than the default
     ck(cudaDeviceSetLimit(cudaLimitStackSize, 4096), "stack limit");
   }
@@ -124,13 +124,21 @@ class CudaBackend final : public Backend {
     // few (large) instances keeps one warp per instance, spread over the SMs
     if (active <= 0 || active > n) active = n;
     if (gang_ > 1) {
-      // one gang block per SM of as many warps as the running instances fill
-      // (up to MFSIM_GANG); thinner than kMinGang warps the one-warp kernel is used
-      const bool forced = gang_min_ >= 0 && active >= gang_min_;
-      const int w = forced ? gang_ : std::min(gang_, active / (sms_ * gang_blocks_));
-      if (forced || w >= min_gang_) {
-        launch_gang(d, order, n, hint, budget, slice_ns, plan, w);
+      // Gang blocks per SM and warps per gang from the running instances: two
+      // gangs of up to 16 warps per SM (a slow warp then holds up half of the
+      // SM), else one gang of up to 32, else the one-warp kernel (A/B,
+      // profiles/r02_gang_ab.txt: 2x16 +5 % over 1x32 at 4736 instances,
+      // 2x9 +8 % over 1x18 at 2800, 1x13 +13 % over one warp each at 2000)
+      if (gang_min_ >= 0 && active >= gang_min_) {  // tests: a gang even for small batches
+        launch_gang(d, order, n, hint, budget, slice_ns, plan, gang_, 1);
         return;
+      }
+      for (int b = gang_blocks_; b >= 1; --b) {
+        const int w = std::min(std::min(gang_, 32 / b), active / (sms_ * b));
+        if (w >= (b > 1 ? min_gang_split_ : min_gang_)) {
+          launch_gang(d, order, n, hint, budget, slice_ns, plan, w, b);
+          return;
+        }
       }
     }
     int per_sm = 0;
@@ -157,12 +165,12 @@ class CudaBackend final : public Backend {
     last_grid_ = grid;
   }
   void launch_gang(const mfb::Inst* d, const int* order, int n, const LaunchHint& hint,
-                   long long budget, long long slice_ns, const mfb::SmemPlan& plan, int w) {
+                   long long budget, long long slice_ns, const mfb::SmemPlan& plan, int w, int blocks) {
     const int threads = 32 * w;
     const int bytes = plan.bytes * w;
     const int per_sm = mfb::gang_kernel_blocks_per_sm(hint.aalo, threads, bytes);
     if (per_sm < 1) throw DeviceError("gang block does not fit an SM");
-    int grid = sms_ * std::min(gang_blocks_, per_sm);  // one gang per SM: its warps share the SM's instruction cache
+    int grid = sms_ * std::min(blocks, per_sm);  // gangs per SM: a gang's warps share the SM's instruction cache
     const int need = (n + w - 1) / w;
     if (need < grid) grid = need > 0 ? need : 1;
     ck(cudaMemsetAsync(counter_ + 1, 0, sizeof(int) * kMaxGroups, stream_), "memset");
@@ -212,7 +220,8 @@ class CudaBackend final : public Backend {
   int* remain_host_ = nullptr;
   int sms_ = 148;
   int gang_ = 32;  // warps per block in lock step (MFSIM_GANG; 1 = one-warp kernel)
-  int gang_blocks_ = 1;  // gang blocks per SM (MFSIM_GANG_BLOCKS, A/B)
+  int gang_blocks_ = 2;  // most gang blocks per SM (MFSIM_GANG_BLOCKS)
+  int min_gang_split_ = 8;  // thinnest gang when an SM holds two
   int min_gang_ = 12;  // thinnest gang worth its barrier (MFSIM_GANG_MINW; A/B: 13 warps +13 %, 9 warps +1 %)
   const char* last_kernel_ = "";
   int gang_min_ = -1;  // fewest instances for a gang launch (-1: a full gang per SM)
