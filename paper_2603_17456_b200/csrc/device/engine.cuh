@@ -152,6 +152,7 @@ struct Sc {
   long long events, steps, streak, pushes, algo_bytes, classes, rounds;
   long long stop_at;  // event count at which this launch suspends
   int pend_ncls;      // classes of a rate recomputation split over gang barriers (-1: none)
+  int pend_kind, pend_a, pend_b;  // the popped event between step_head and step_dispatch
   bool pend_caps;
   int n_flows, n_batches, n_coflows, n_active, n_ev;
   int rp_top, pp_top, cm_top;
@@ -3202,6 +3203,11 @@ MF_UNROLL
   }
   // the event itself: pop, advance, dispatch; leaves s.dirty for settle()
   MF_NOINLINE int step_event(unsigned long long deadline_ns) {
+    const int r = step_head(deadline_ns);
+    return r ? r : step_dispatch();
+  }
+  // pop the next event and advance the active flows to its time
+  MF_NOINLINE int step_head(unsigned long long deadline_ns) {
     if (s.err) return 1;
     if (s.events >= s.stop_at) return 2;
     if (deadline_ns && now_ns() >= deadline_ns) return 2;
@@ -3243,6 +3249,14 @@ MF_UNROLL
       s.streak = 0;
       s.prev_t = e.t;
     }
+    s.pend_kind = kind;
+    s.pend_a = a;
+    s.pend_b = b;
+    return 0;
+  }
+  // the popped event's handler (engine.cpp:613-650)
+  MF_NOINLINE int step_dispatch() {
+    const int kind = s.pend_kind, a = s.pend_a, b = s.pend_b;
     MF_TIC(th);
     switch (kind) {
       case EV_FLOW: {

@@ -67,7 +67,11 @@ __global__ void __launch_bounds__(1024, 1)
 #if defined(MF_GANG_PROF)
       const long long b0 = clock64();
 #endif
+#if defined(MF_GANG_SPLIT4)
+      int r = eng.step_head(deadline);
+#else
       const int r = eng.step_event(deadline);
+#endif
 #if defined(MF_GANG_PROF)
       busy += clock64() - b0;
       ++n_it;
@@ -79,6 +83,17 @@ __global__ void __launch_bounds__(1024, 1)
         state = 0;
       }
     }
+#if defined(MF_GANG_SPLIT4)
+    __syncthreads();
+    if (state == 1) {
+      if (eng.step_dispatch() != 0) {
+        const bool done = eng.end(true);
+        if (done && lane == 0) atomicSub(remaining, 1);
+        __syncwarp();
+        state = 0;
+      }
+    }
+#endif
     // barriers between the event, the policy classes, the filling and the
     // completion events: the gang's warps run each phase's code together
     __syncthreads();
