@@ -8,13 +8,13 @@ namespace mfb {
 
 // Gang variant: a block of W warps, each owning its own instance (and its own
 // slice of shared memory), advances all W instances ONE EVENT at a time in
-// lock step, with a block barrier between the event, its policy classes, its
-// filling and its completion events. The engine is instruction-fetch bound
+// lock step, with a block barrier between popping the event, its handler, its
+// policy classes, its filling and its completion events. The engine is instruction-fetch bound
 // (ncu: 50-68 % of warp stalls "no instruction", ~40k SASS instructions, warps
 // of one SM in different phases); in lock step the W warps of a block run
 // through the same code at about the same time (A/B, profiles/r02_gang_ab.txt:
-// one barrier per event +13-15 %, the three phase barriers another +2.5 %,
-// two events per barrier -17 %).
+// one barrier per event +13-15 %, the phase barriers another +3 %, two
+// events per barrier -17 %, two 16-warp gangs per SM +5 % over one of 32).
 template <bool kAalo>
 __global__ void __launch_bounds__(1024, 1)
     mfsim_gang_kernel(const Inst* __restrict__ insts, const int* __restrict__ order, int n,
@@ -67,11 +67,7 @@ __global__ void __launch_bounds__(1024, 1)
 #if defined(MF_GANG_PROF)
       const long long b0 = clock64();
 #endif
-#if defined(MF_GANG_SPLIT4)
-      int r = eng.step_head(deadline);
-#else
-      const int r = eng.step_event(deadline);
-#endif
+      const int r = eng.step_head(deadline);
 #if defined(MF_GANG_PROF)
       busy += clock64() - b0;
       ++n_it;
@@ -83,7 +79,9 @@ __global__ void __launch_bounds__(1024, 1)
         state = 0;
       }
     }
-#if defined(MF_GANG_SPLIT4)
+    // barriers between popping the event, its handler, the policy classes,
+    // the filling and the completion events: the gang's warps run each
+    // phase's code together
     __syncthreads();
     if (state == 1) {
       if (eng.step_dispatch() != 0) {
@@ -93,9 +91,6 @@ __global__ void __launch_bounds__(1024, 1)
         state = 0;
       }
     }
-#endif
-    // barriers between the event, the policy classes, the filling and the
-    // completion events: the gang's warps run each phase's code together
     __syncthreads();
 #if defined(MF_GANG_PROF)
     long long b1 = clock64();
