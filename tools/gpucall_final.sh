@@ -1,11 +1,12 @@
-# GPU call: final product -- gpu tests, smoke, default bench, ncu launch list + full capture
-mkdir -p gpurun_out
-timeout 1200 python -m pytest tests -m gpu -x -q --durations=4 > gpurun_out/pytest_final.log 2>&1; echo "pytest=$?"
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_final.log 2>&1; echo "smoke=$?"
-timeout 900 python bench.py > gpurun_out/bench_final.json 2> gpurun_out/bench_final.err; echo "bench=$?"
-B="python bench.py --steps 3 --warmup 3 --no-cpu-baseline"
-timeout 600 $B > gpurun_out/bench_final_nocpu.json 2> gpurun_out/bench_final_nocpu.err && \
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_final.csv $B > gpurun_out/ncu_launch_final.log 2>&1; echo "ncu_launch=$?"
-timeout 300 python tools/profile_batch.py 4736 2000 200 > gpurun_out/pb_final_plain.log 2>&1 && \
-timeout 1200 ncu --profile-from-start off --set full --clock-control none --import-source on -k regex:mfsim_engine -c 1 -o gpurun_out/prof_final_engine python tools/profile_batch.py 4736 2000 200 > gpurun_out/ncu_final_full.log 2>&1; echo "ncu_full=$?"
-tail -4 gpurun_out/pytest_final.log; cat gpurun_out/smoke_final.log gpurun_out/bench_final.json gpurun_out/pb_final_plain.log
+#!/bin/bash
+# round-2 final build: GPU tier, smoke, bench, launch list
+python -m pytest tests -m gpu -q > gpurun_out/final_pytest_gpu.log 2>&1; echo "pytest_rc=$?" >> gpurun_out/final_pytest_gpu.log
+tail -2 gpurun_out/final_pytest_gpu.log
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/final_smoke.log 2>&1; echo "smoke_rc=$?" >> gpurun_out/final_smoke.log
+cat gpurun_out/final_smoke.log
+python bench.py > gpurun_out/final_bench.json 2> gpurun_out/final_bench.err; echo "bench_rc=$?"
+cat gpurun_out/final_bench.json
+python bench.py --steps 2 --warmup 1 --no-cpu-baseline > gpurun_out/final_bench_short.json 2>&1 && \
+ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file gpurun_out/final_launches.csv \
+  python bench.py --steps 2 --warmup 1 --no-cpu-baseline > gpurun_out/final_ncu_launches.log 2>&1
+echo "ncu_launches_rc=$?"
