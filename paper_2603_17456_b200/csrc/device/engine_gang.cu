@@ -9,10 +9,11 @@ namespace mfb {
 // Gang variant: a block of W warps, each owning its own instance (and its own
 // slice of shared memory), advances all W instances ONE EVENT at a time in
 // lock step, with a block barrier between popping the event, its handler, its
-// policy classes, its filling and its completion events. The engine is instruction-fetch bound
-// (ncu: 50-68 % of warp stalls "no instruction", ~40k SASS instructions, warps
-// of one SM in different phases); in lock step the W warps of a block run
-// through the same code at about the same time (A/B, profiles/r02_gang_ab.txt:
+// policy classes, its filling and its completion events. The engine is
+// instruction-fetch bound (ncu: 50-68 % of warp stalls "no instruction", ~40k
+// SASS instructions, warps of one SM in different phases); in lock step the W
+// warps of a block run through the same code at about the same time (A/B,
+// profiles/r02_gang_ab.txt:
 // one barrier per event +13-15 %, the phase barriers another +3 %, two
 // events per barrier -17 %, two 16-warp gangs per SM +5 % over one of 32).
 template <bool kAalo>
@@ -83,6 +84,9 @@ __global__ void __launch_bounds__(1024, 1)
     // the filling and the completion events: the gang's warps run each
     // phase's code together
     __syncthreads();
+#if defined(MF_GANG_PROF)
+    long long b1 = clock64();
+#endif
     if (state == 1) {
       if (eng.step_dispatch() != 0) {
         const bool done = eng.end(true);
@@ -91,9 +95,12 @@ __global__ void __launch_bounds__(1024, 1)
         state = 0;
       }
     }
+#if defined(MF_GANG_PROF)
+    busy += clock64() - b1;
+#endif
     __syncthreads();
 #if defined(MF_GANG_PROF)
-    long long b1 = clock64();
+    b1 = clock64();
 #endif
     if (state == 1) eng.settle_decide();
 #if defined(MF_GANG_PROF)
