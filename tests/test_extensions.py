@@ -255,3 +255,27 @@ def test_varys_device_matches_oracle(product):
         if d:
             bad[i] = d
     assert bad == {}
+
+
+@pytest.mark.gpu
+def test_extensions_under_the_gang_kernel(product):
+    """the extension kernel instance (aalo / varys code compiled in) as a
+    lock-step gang: forced for this small batch, same results as the oracle"""
+    from paper_2603_17456_b200.native import DeviceBatch
+    texts = list(aalo_cases().values())[:3] + list(varys_cases().values())[:3]
+    os.environ["MFSIM_GANG_MIN"] = "1"
+    try:
+        b = DeviceBatch(0, product)
+    finally:
+        os.environ.pop("MFSIM_GANG_MIN", None)
+    for t in texts:
+        b.add_config(t)
+    b.prepare()
+    b.run(2)
+    assert b.last_kernel == "mfsim_gang_kernel"
+    bad = {}
+    for i, t in enumerate(texts):
+        d = diff(b.result(i, 2, reports=True), ref.run_config(t, so=ref.ORACLE_SO))
+        if d:
+            bad[i] = d
+    assert bad == {}
