@@ -153,9 +153,6 @@ struct Sc {
   long long stop_at;  // event count at which this launch suspends
   int pend_ncls;      // classes of a rate recomputation split over gang barriers (-1: none)
   int pend_kind, pend_a, pend_b;  // the popped event between step_head and step_dispatch
-  bool ct_ok;       // capped filling: ct_c2 / ct_p1 / ct_p2 hold the last pass's two smallest caps
-  int ct_p1, ct_p2;
-  double ct_c2;
   bool pend_caps;
   int n_flows, n_batches, n_coflows, n_active, n_ev;
   int rp_top, pp_top, cm_top;
@@ -1870,9 +1867,6 @@ MF_UNROLL
         ncap += popc32(mc);
       }
       cmn = g.min_nonneg(cmn);  // smax(0, cap) >= 0
-#if defined(MF_CAP_TOP2)
-      s.ct_ok = false;  // the first round makes a full pass
-#endif
       g.sync();
       {  // slot -> member incidence: extents from the counts, atomic fill
         int off = 0;
@@ -2009,49 +2003,9 @@ MF_UNROLL
         // cap freezes (the same rate R, so the order against the link freezes
         // is immaterial): drop frozen entries, freeze cap - eps <= R, and take
         // the minimum cap of the survivors for the next round
-#if defined(MF_CAP_TOP2)
-        // The two smallest live caps of the last full pass (cmn at member
-        // ct_p1, ct_c2 at ct_p2; every other live cap >= ct_c2) settle a
-        // round without a pass when it freezes at most that first member.
-        bool cap_scan = ncap > 0;
-        if (ncap > 0 && s.ct_ok) {
-          const double c2 = s.ct_c2;
-          if (!(c2 < MF_INF && R >= dsub(c2, dmul(1e-12, smax(1.0, c2))))) {
-            const int p1 = s.ct_p1;
-            const bool live1 = !(frz[p1 >> 5] & (1u << (p1 & 31)));
-            const bool fz1 = live1 && R >= dsub(cmn, dmul(1e-12, smax(1.0, cmn)));
-            if (fz1) {
-              g.sync();
-              if (g.leader()) {
-                g.atomic_or(&frz[p1 >> 5], 1u << (p1 & 31));
-                rate[p1] = R;
-                route_slots_add(cnt, asl + p1 * RM, arnp[p1], -1);
-                ++got;
-              }
-              g.sync();
-            }
-            if (live1 && !fz1) {
-              cap_scan = false;  // the minimum stays at p1
-            } else {
-              const int p2 = s.ct_p2;
-              if (!(c2 < MF_INF) || !(frz[p2 >> 5] & (1u << (p2 & 31)))) {
-                cmn = c2;  // the runner-up is the new minimum (none left: +inf)
-                s.ct_ok = false;
-                cap_scan = false;
-              }
-            }
-          }
-        }
-        if (cap_scan) {
-#else
         if (ncap > 0) {
-#endif
           int nc2 = 0;
           double mn = MF_INF;
-#if defined(MF_CAP_TOP2)
-          double a2 = MF_INF;
-          int q1 = 0, q2 = 0;
-#endif
           for (int base = 0; base < ncap; base += G::N) {
             const int i = base + g.lane();
             bool keep = false, fz = false;
@@ -2078,43 +2032,11 @@ MF_UNROLL
               const int slot = nc2 + popc32(mk & g.lanemask_lt());
               I.x_hi[slot] = dbits(cp);
               I.x_lo[slot] = (unsigned long long)p;
-#if defined(MF_CAP_TOP2)
-              if (cp < mn) {
-                a2 = mn;
-                q2 = q1;
-                mn = cp;
-                q1 = p;
-              } else if (cp < a2) {
-                a2 = cp;
-                q2 = p;
-              }
-#else
               mn = smin(mn, cp);
-#endif
             }
             nc2 += popc32(mk);
           }
-#if defined(MF_CAP_TOP2)
-          const double lm = mn;
-#endif
           mn = g.min_nonneg(mn);  // stored caps are smax(0, cap) >= 0
-#if defined(MF_CAP_TOP2)
-          {  // warp runner-up: the winner lane offers its second, the others their first
-            const unsigned wm = g.ballot(lm == mn);
-            const int w = ctz32(wm);
-            const int p1 = g.shfl(q1, w);
-            const bool win = g.lane() == w;
-            const double cand = win ? a2 : lm;
-            const int candp = win ? q2 : q1;
-            const double c2 = g.min_nonneg(cand);
-            const int w2 = ctz32(g.ballot(cand == c2));
-            const int p2 = g.shfl(candp, w2);
-            s.ct_ok = mn < MF_INF;
-            s.ct_c2 = c2;
-            s.ct_p1 = p1;
-            s.ct_p2 = p2;
-          }
-#endif
           g.sync();
           ncap = nc2;
           cmn = mn;
